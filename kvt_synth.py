@@ -1,0 +1,77 @@
+"""Seeded synthetic inputs shared by the oracle tests, the GPU parity tests and bench.py.
+
+This module holds NO arithmetic of the method (no quantisation, no attention): only random
+tensors with the shapes and value distributions of the paper's workloads:
+
+* K ~ N(0, 1) with channels c ≡ 0 (mod 8) scaled ×11 — the key channel outliers the paper
+  cites ("key cache has strong channel-wise outliers"; recipe of S:62).
+* V ~ N(0, 1).
+* q ~ 0.5·N(0, 1) (logit std ≈ 2 at d = 128 with the outlier channels).
+* Optional attention-sink heads: q aligned with k_0 on a fraction of the heads.
+
+All generators take an explicit seed and a device; tensors are bf16 ("BF16 KV cache").
+"""
+from __future__ import annotations
+
+import torch
+
+OUTLIER_PERIOD = 8
+OUTLIER_SCALE = 11.0
+
+
+def generator(seed: int, device="cpu") -> torch.Generator:
+    g = torch.Generator(device=device)
+    g.manual_seed(int(seed))
+    return g
+
+
+def keys(shape, seed: int, device="cpu", outliers: bool = True) -> torch.Tensor:
+    """bf16 keys with channel outliers on the last dim (c % 8 == 0 scaled ×11)."""
+    g = generator(seed, device)
+    x = torch.randn(*shape, generator=g, device=device, dtype=torch.float32)
+    if outliers:
+        x[..., ::OUTLIER_PERIOD] *= OUTLIER_SCALE
+    return x.to(torch.bfloat16)
+
+
+def values(shape, seed: int, device="cpu") -> torch.Tensor:
+    g = generator(seed, device)
+    return torch.randn(*shape, generator=g, device=device, dtype=torch.float32).to(torch.bfloat16)
+
+
+def queries(shape, seed: int, device="cpu", std: float = 0.5) -> torch.Tensor:
+    g = generator(seed, device)
+    return (std * torch.randn(*shape, generator=g, device=device, dtype=torch.float32)).to(torch.bfloat16)
+
+
+def ragged_lengths(batch: int, lo: int, hi: int, seed: int) -> torch.Tensor:
+    """int32 lengths uniform in [lo, hi] (host)."""
+    g = generator(seed, "cpu")
+    return torch.randint(lo, hi + 1, (batch,), generator=g, dtype=torch.int32)
+
+
+def special_rows(kind: str, shape, seed: int) -> torch.Tensor:
+    """Edge-case bf16 tensors (host): 'constant', 'grid' (values on a quantisation grid, ties),
+    'zeros', 'tiny' (values near the bf16 subnormal range), 'wide' (|x| up to 1e4)."""
+    g = generator(seed, "cpu")
+    if kind == "constant":
+        v = torch.randn((), generator=g).item()
+        return torch.full(shape, v, dtype=torch.float32).to(torch.bfloat16)
+    if kind == "zeros":
+        return torch.zeros(shape, dtype=torch.bfloat16)
+    if kind == "grid":
+        base = torch.randint(0, 16, shape, generator=g).to(torch.float32)
+        return (0.25 * base - 1.0).to(torch.bfloat16)
+    if kind == "tiny":
+        return (1e-30 * torch.randn(*shape, generator=g)).to(torch.bfloat16)
+    if kind == "wide":
+        return (1e4 * torch.randn(*shape, generator=g)).to(torch.bfloat16)
+    raise ValueError(kind)
+
+
+def bf16_bits(t: torch.Tensor):
+    """Raw bf16 bits of a (CPU or CUDA) bf16 tensor as a numpy uint16 array (host)."""
+    import numpy as np
+
+    assert t.dtype == torch.bfloat16
+    return t.detach().contiguous().cpu().view(torch.int16).numpy().view(np.uint16)
