@@ -1,0 +1,12 @@
+"""B200-native KVTuner hot path (arXiv 2502.04420): layer-wise mixed-precision KV-cache
+quantisation and the decode attention that reads it.  The compute lives in libkvt.so (sm_100a
+CUDA, C ABI in include/kvt.h); this package is its thin Python binding."""
+from .kvt import (ABI_VERSION, BUFFER_NAMES, ERROR_NAMES, MODE_KIVI, MODE_PER_TOKEN_ASYM, Config, KvtError,
+                  LayerCache, LayerSpec, cache_buffer_sizes, combine_partials, decode_attention,
+                  decode_attention_partial, decode_workspace_bytes, layer_sensitivity, lib, load_config,
+                  quantize_append, validate_spec)
+
+__all__ = ["ABI_VERSION", "BUFFER_NAMES", "ERROR_NAMES", "MODE_KIVI", "MODE_PER_TOKEN_ASYM", "Config", "KvtError",
+           "LayerCache", "LayerSpec", "cache_buffer_sizes", "combine_partials", "decode_attention",
+           "decode_attention_partial", "decode_workspace_bytes", "layer_sensitivity", "lib", "load_config",
+           "quantize_append", "validate_spec"]

@@ -1,0 +1,180 @@
+// kvt_decode.cu — launch planning for K2 (split-KV decode attention) and K3 (combine).
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <mutex>
+
+#include "kvt_decode.cuh"
+
+namespace kvt {
+namespace dec {
+using KFn = void (*)(DecodeArgs);
+KFn get_decode_k2(int VB, bool KPC, int GM);
+KFn get_decode_k4(int VB, bool KPC, int GM);
+KFn get_decode_k8(int VB, bool KPC, int GM);
+KFn get_decode_k16(int VB, bool KPC, int GM);
+
+// K3: merge n_parts partial rows [n_parts][rows][2 + D] -> out (bf16 / fp32 / partial).  One warp
+// per row; lane owns 4 channels.
+__global__ void __launch_bounds__(128) combine_kernel(const float* __restrict__ parts, int n_parts, int rows,
+                                                      void* out, int out_mode) {
+    const int row = blockIdx.x * 4 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    float M = -INFINITY;
+    for (int j = 0; j < n_parts; ++j) M = fmaxf(M, parts[((size_t)j * rows + row) * (2 + D)]);
+    float L = 0.0f;
+    float o[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    if (M != -INFINITY) {
+        for (int j = 0; j < n_parts; ++j) {
+            const float* pr = parts + ((size_t)j * rows + row) * (2 + D);
+            float wgt = pr[1] * exp2f(pr[0] - M);
+            if (wgt == 0.0f) continue;
+            L += wgt;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) o[i] += wgt * pr[2 + 4 * lane + i];
+        }
+    }
+    if (out_mode == 2) {
+        float* pr = reinterpret_cast<float*>(out) + (size_t)row * (2 + D);
+        if (lane == 0) { pr[0] = M; pr[1] = L; }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) pr[2 + 4 * lane + i] = L > 0.0f ? __fdiv_rn(o[i], L) : 0.0f;
+        return;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        float v = L > 0.0f ? __fdiv_rn(o[i], L) : 0.0f;
+        if (out_mode == 1) reinterpret_cast<float*>(out)[(size_t)row * D + 4 * lane + i] = v;
+        else reinterpret_cast<__nv_bfloat16*>(out)[(size_t)row * D + 4 * lane + i] = __float2bfloat16_rn(v);
+    }
+}
+
+
+static size_t smem_bytes(int VB, int GM) {
+    auto pick = [&](auto gm_tag) -> size_t {
+        constexpr int GMv = decltype(gm_tag)::value;
+        switch (VB) {
+            case 2: return Smem<GMv, 2>::bytes;
+            case 4: return Smem<GMv, 4>::bytes;
+            case 8: return Smem<GMv, 8>::bytes;
+            default: return Smem<GMv, 16>::bytes;
+        }
+    };
+    return GM == 4 ? pick(std::integral_constant<int, 4>{}) : pick(std::integral_constant<int, 8>{});
+}
+
+struct Instance {
+    KFn fn = nullptr;
+    size_t smem = 0;
+    int occ = 1;
+};
+
+static int bits_index(int b) { return b == 2 ? 0 : b == 4 ? 1 : b == 8 ? 2 : 3; }
+
+// Per-device cache of (function, smem, occupancy) for each instance; configured once.
+static std::mutex g_mu;
+static Instance g_inst[8][4][4][2][2];   // [device][kb][vb][kpc][gm]
+static bool g_ready[8][4][4][2][2];
+static int g_sms[8];
+
+static int32_t get_instance(int kb, int vb, bool kpc, int GM, Instance* out, int* sms) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 8) return fail(KVT_ERR_CUDA, "cudaGetDevice failed");
+    int ki = bits_index(kb), vi = bits_index(vb), pi = kpc ? 1 : 0, gi = GM == 4 ? 0 : 1;
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g_ready[dev][ki][vi][pi][gi]) {
+        Instance in;
+        switch (kb) {
+            case 2: in.fn = get_decode_k2(vb, kpc, GM); break;
+            case 4: in.fn = get_decode_k4(vb, kpc, GM); break;
+            case 8: in.fn = get_decode_k8(vb, kpc, GM); break;
+            default: in.fn = get_decode_k16(vb, kpc, GM); break;
+        }
+        in.smem = smem_bytes(vb, GM);
+        cudaError_t e = cudaFuncSetAttribute(in.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)in.smem);
+        if (e != cudaSuccess) return fail(KVT_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&in.occ, in.fn, kThreads, in.smem);
+        if (e != cudaSuccess || in.occ < 1) in.occ = 1;
+        if (!g_sms[dev]) {
+            int n = 0;
+            cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+            g_sms[dev] = n > 0 ? n : 148;
+        }
+        g_inst[dev][ki][vi][pi][gi] = in;
+        g_ready[dev][ki][vi][pi][gi] = true;
+    }
+    *out = g_inst[dev][ki][vi][pi][gi];
+    *sms = g_sms[dev];
+    return KVT_OK;
+}
+
+// Number of KV splits: enough CTAs for ~4 waves of resident CTAs, at least 16 tiles per split.
+static int plan_splits(const Geometry& g, int plan_len, int occ, int sms) {
+    int n_tiles = (plan_len + kTile - 1) / kTile;
+    long long base = (long long)g.B * g.H;
+    long long target = 4LL * sms * occ;
+    int n = (int)((target + base - 1) / base);
+    int max_by_len = n_tiles / 16;
+    if (n > max_by_len) n = max_by_len;
+    if (n < 1) n = 1;
+    if (n > 64) n = 64;
+    return n;
+}
+
+}  // namespace dec
+
+size_t decode_workspace(const Geometry& g, int H_q, int plan_len) {
+    using namespace dec;
+    int GM = (H_q / g.H) <= 4 ? 4 : 8;
+    Instance in; int sms = 148;
+    if (get_instance(g.kb, g.vb, g.key_per_channel, GM, &in, &sms) != KVT_OK) { in.occ = 4; sms = 148; }
+    int ns = plan_splits(g, plan_len, in.occ, sms);
+    return ns > 1 ? (size_t)ns * g.B * H_q * (D + 2) * sizeof(float) : 0;
+}
+
+int32_t launch_decode(const Geometry& g, const CachePtrs& c, const uint16_t* q, int H_q, const int32_t* seq_len,
+                      int plan_len, float scale, void* out, int out_mode, void* workspace, size_t ws_bytes,
+                      void* stream) {
+    using namespace dec;
+    const int gq = H_q / g.H;
+    const int GM = gq <= 4 ? 4 : 8;
+    Instance in; int sms = 148;
+    int32_t st = get_instance(g.kb, g.vb, g.key_per_channel, GM, &in, &sms);
+    if (st) return st;
+    int ns = plan_splits(g, plan_len, in.occ, sms);
+    size_t need = ns > 1 ? (size_t)ns * g.B * H_q * (D + 2) * sizeof(float) : 0;
+    if (need > ws_bytes || (need && !workspace))
+        return fail(KVT_ERR_WORKSPACE, "decode: workspace %zu < %zu bytes (use kvt_decode_workspace_bytes)", ws_bytes, need);
+    if (g.B > 65535 || g.H > 65535) return fail(KVT_ERR_UNSUPPORTED, "decode: batch/heads exceed grid limits");
+    DecodeArgs a;
+    a.g = g; a.c = c; a.q = q; a.H_q = H_q; a.gq = gq; a.seq_len = seq_len;
+    a.scale_log2 = scale * 1.4426950408889634f;
+    a.out = out;
+    a.out_mode = ns > 1 ? 3 : out_mode;
+    a.parts = (float*)workspace;
+    a.n_split = ns;
+    dim3 grid(ns, g.H, g.B);
+    in.fn<<<grid, kThreads, in.smem, (cudaStream_t)stream>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(KVT_ERR_CUDA, "decode launch: %s", cudaGetErrorString(e));
+    if (ns > 1) {
+        int rows = g.B * H_q;
+        combine_kernel<<<(rows + 3) / 4, 128, 0, (cudaStream_t)stream>>>((const float*)workspace, ns, rows, out, out_mode);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return fail(KVT_ERR_CUDA, "combine launch: %s", cudaGetErrorString(e));
+    }
+    return KVT_OK;
+}
+
+int32_t launch_combine(const float* parts, int n_parts, int B, int H_q, int d, void* out, int out_dtype, void* stream) {
+    using namespace dec;
+    (void)d;
+    int rows = B * H_q;
+    combine_kernel<<<(rows + 3) / 4, 128, 0, (cudaStream_t)stream>>>(parts, n_parts, rows, out, out_dtype);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(KVT_ERR_CUDA, "combine launch: %s", cudaGetErrorString(e));
+    return KVT_OK;
+}
+
+}  // namespace kvt

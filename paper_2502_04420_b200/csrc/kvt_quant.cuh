@@ -1,0 +1,90 @@
+// kvt_quant.cuh — the Eq. 2 group quantiser shared by K1 (append) and K5 (sensitivity).
+// Readings A1-A4: exact min/max, IEEE fp32 s32 = (max-min)/(2^b-1), bf16 scale rounded
+// toward +inf, inv = 1/scale, t = (x - z) * inv without FMA contraction, code = clamp(rint(t)).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace kvt {
+namespace quant {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ float bf2f(uint32_t b16) { return __uint_as_float(b16 << 16); }
+
+__device__ __forceinline__ uint32_t bf16_ru_bits(float f) {
+    return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_ru(f));
+}
+
+// Eq. 2 statistics of one group -> (scale bits, zero bits, inverse scale, degenerate?)
+struct GroupQ {
+    uint32_t s_bits, z_bits;
+    float mn, inv, qmax;
+    bool degenerate;
+};
+
+__device__ __forceinline__ GroupQ group_params(float mn, float mx, int bits) {
+    GroupQ q;
+    if (mn == 0.0f) mn = 0.0f;                      // canonical +0 zero-point (A3)
+    q.mn = mn;
+    q.z_bits = __float_as_uint(mn) >> 16;           // exact: mn is a bf16 value
+    q.qmax = (float)((1 << bits) - 1);
+    q.degenerate = (mx == mn);
+    if (q.degenerate) {                             // A2: s := 1, codes 0
+        q.s_bits = 0x3F80u;
+        q.inv = 0.0f;
+    } else {
+        float s32 = __fdiv_rn(__fsub_rn(mx, mn), q.qmax);
+        q.s_bits = bf16_ru_bits(s32);
+        q.inv = __fdiv_rn(1.0f, bf2f(q.s_bits));
+    }
+    return q;
+}
+
+__device__ __forceinline__ uint32_t code_of(float x, const GroupQ& q) {
+    if (q.degenerate) return 0u;
+    float t = __fmul_rn(__fsub_rn(x, q.mn), q.inv);
+    float r = rintf(t);
+    r = fmaxf(r, 0.0f);
+    r = fminf(r, q.qmax);
+    return (uint32_t)r;
+}
+
+__device__ __forceinline__ void unpack4(uint2 v, float x[4]) {
+    x[0] = bf2f(v.x & 0xffffu); x[1] = bf2f(v.x >> 16);
+    x[2] = bf2f(v.y & 0xffffu); x[3] = bf2f(v.y >> 16);
+}
+
+__device__ __forceinline__ void store_packed(uint8_t* row, int lane, int bits, uint32_t packed) {
+    if (bits == 2) row[lane] = (uint8_t)packed;
+    else if (bits == 4) reinterpret_cast<uint16_t*>(row)[lane] = (uint16_t)packed;
+    else reinterpret_cast<uint32_t*>(row)[lane] = packed;
+}
+
+// Quantise one 128-channel token row held as 4 bf16 per lane; per-token groups of G channels.
+__device__ __forceinline__ void quant_row_warp(uint2 xv, int bits, int G, uint8_t* row, uint32_t* meta_row, int lane) {
+    if (bits == 16) {                                // bf16 pass-through
+        reinterpret_cast<uint2*>(row)[lane] = xv;
+        return;
+    }
+    float x[4];
+    unpack4(xv, x);
+    float mn = fminf(fminf(x[0], x[1]), fminf(x[2], x[3]));
+    float mx = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
+    for (int off = 1; off < G / 4; off <<= 1) {       // the G/4 lanes of one group
+        mn = fminf(mn, __shfl_xor_sync(kFull, mn, off));
+        mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, off));
+    }
+    GroupQ q = group_params(mn, mx, bits);
+    uint32_t packed = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) packed |= code_of(x[i], q) << (i * bits);
+    store_packed(row, lane, bits, packed);
+    if ((lane & (G / 4 - 1)) == 0) meta_row[lane / (G / 4)] = q.s_bits | (q.z_bits << 16);
+}
+
+
+}  // namespace quant
+}  // namespace kvt

@@ -1,0 +1,330 @@
+"""Thin Python binding of libkvt.so (include/kvt.h) — argument marshalling only.
+
+Every step of the hot path runs in the library's sm_100a kernels; this module only checks torch
+tensors (dtype, device, contiguity), passes raw pointers and the current CUDA stream through
+ctypes, and raises ``KvtError`` with the library's message on a non-zero status.  There is no CPU
+fallback: if ``libkvt.so`` is missing, importing this module fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+from pathlib import Path
+from typing import Optional, Sequence
+
+import torch
+
+_LIB_PATH = Path(__file__).resolve().parent / "libkvt.so"
+
+MODE_PER_TOKEN_ASYM = 0
+MODE_KIVI = 1
+_MODE_NAMES = {"per-token-asym": MODE_PER_TOKEN_ASYM, "kivi": MODE_KIVI}
+
+
+class KvtError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"kvt status {status}: {msg}")
+        self.status = status
+
+
+class _Spec(ctypes.Structure):
+    _fields_ = [("mode", ctypes.c_int32), ("key_bits", ctypes.c_int32), ("value_bits", ctypes.c_int32),
+                ("group", ctypes.c_int32), ("residual", ctypes.c_int32)]
+
+
+class _Cache(ctypes.Structure):
+    _fields_ = [("spec", _Spec), ("batch", ctypes.c_int32), ("kv_heads", ctypes.c_int32),
+                ("head_dim", ctypes.c_int32), ("capacity", ctypes.c_int32),
+                ("k_codes", ctypes.c_void_p), ("k_meta", ctypes.c_void_p), ("k_resid", ctypes.c_void_p),
+                ("v_codes", ctypes.c_void_p), ("v_meta", ctypes.c_void_p), ("v_resid", ctypes.c_void_p)]
+
+
+class _Pair(ctypes.Structure):
+    _fields_ = [("key_bits", ctypes.c_int32), ("value_bits", ctypes.c_int32)]
+
+
+def _load():
+    if not _LIB_PATH.exists():
+        raise ImportError(f"{_LIB_PATH} is missing: build it with `python -m paper_2502_04420_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(str(_LIB_PATH))
+    P, i32, u64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint64
+    sig = {
+        "kvt_abi_version": (ctypes.c_uint32, []),
+        "kvt_status_string": (ctypes.c_char_p, [i32]),
+        "kvt_last_error": (ctypes.c_char_p, []),
+        "kvt_config_load": (i32, [ctypes.c_char_p, ctypes.POINTER(P)]),
+        "kvt_config_num_layers": (i32, [P]),
+        "kvt_config_layer": (i32, [P, i32, ctypes.POINTER(_Spec)]),
+        "kvt_config_equivalent_bits": (ctypes.c_double, [P]),
+        "kvt_config_label_bits": (ctypes.c_double, [P]),
+        "kvt_config_model_name": (ctypes.c_char_p, [P]),
+        "kvt_config_free": (None, [P]),
+        "kvt_validate_spec": (i32, [ctypes.POINTER(_Spec), i32]),
+        "kvt_cache_buffer_sizes": (i32, [ctypes.POINTER(_Spec), i32, i32, i32, i32, ctypes.POINTER(u64)]),
+        "kvt_quantize_append": (i32, [ctypes.POINTER(_Cache), P, P, ctypes.POINTER(ctypes.c_int64), P, P, P, P,
+                                      i32, P]),
+        "kvt_decode_workspace_bytes": (i32, [ctypes.POINTER(_Cache), i32, P, ctypes.POINTER(u64)]),
+        "kvt_decode_attention": (i32, [ctypes.POINTER(_Cache), P, i32, P, P, ctypes.c_float, P, i32, P, u64, P]),
+        "kvt_decode_attention_partial": (i32, [ctypes.POINTER(_Cache), P, i32, P, P, ctypes.c_float, P, P, u64,
+                                               P]),
+        "kvt_combine_partials": (i32, [P, i32, i32, i32, i32, P, i32, P]),
+        "kvt_sensitivity_workspace_bytes": (i32, [i32, i32, i32, i32, i32, i32, ctypes.POINTER(u64)]),
+        "kvt_layer_sensitivity": (i32, [i32, i32, i32, P, i32, i32, i32, P, P, i32, i32, i32, ctypes.c_float,
+                                        ctypes.POINTER(_Pair), i32, P, P, u64, P]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+_lib = _load()
+ABI_VERSION = int(_lib.kvt_abi_version())
+EXPORTED = ("kvt_abi_version", "kvt_status_string", "kvt_last_error", "kvt_config_load", "kvt_config_num_layers",
+            "kvt_config_layer", "kvt_config_equivalent_bits", "kvt_config_label_bits", "kvt_config_model_name",
+            "kvt_config_free", "kvt_validate_spec", "kvt_cache_buffer_sizes", "kvt_quantize_append",
+            "kvt_decode_workspace_bytes", "kvt_decode_attention", "kvt_decode_attention_partial",
+            "kvt_combine_partials", "kvt_sensitivity_workspace_bytes", "kvt_layer_sensitivity")
+
+
+def lib():
+    return _lib
+
+
+def _check(status: int):
+    if status != 0:
+        raise KvtError(status, _lib.kvt_last_error().decode())
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _dev(t: torch.Tensor, name: str, dtype=None):
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if dtype is not None and t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    return t
+
+
+def _host_i32(t) -> Optional[ctypes.Array]:
+    if t is None:
+        return None
+    vals = [int(v) for v in (t.tolist() if isinstance(t, torch.Tensor) else t)]
+    return (ctypes.c_int32 * len(vals))(*vals)
+
+
+# ------------------------------------------------------------------------------------------------
+# a1: configuration
+# ------------------------------------------------------------------------------------------------
+@dataclass(frozen=True)
+class LayerSpec:
+    mode: int
+    key_bits: int
+    value_bits: int
+    group: int = 32
+    residual: int = 0
+
+    def _c(self) -> _Spec:
+        return _Spec(self.mode, self.key_bits, self.value_bits, self.group, self.residual)
+
+    @staticmethod
+    def kivi(key_bits, value_bits, group=32, residual=32):
+        return LayerSpec(MODE_KIVI, key_bits, value_bits, group, residual)
+
+    @staticmethod
+    def per_token(key_bits, value_bits, group=32, residual=0):
+        return LayerSpec(MODE_PER_TOKEN_ASYM, key_bits, value_bits, group, residual)
+
+
+class Config:
+    """A searched layer-wise configuration (kvt_config_load)."""
+
+    def __init__(self, path_or_json: str):
+        h = ctypes.c_void_p()
+        _check(_lib.kvt_config_load(str(path_or_json).encode(), ctypes.byref(h)))
+        self._h = h
+        self.num_layers = int(_lib.kvt_config_num_layers(h))
+        self.equivalent_bits = float(_lib.kvt_config_equivalent_bits(h))
+        self.label_bits = float(_lib.kvt_config_label_bits(h))
+        self.model_name = _lib.kvt_config_model_name(h).decode()
+        self.layers = []
+        for i in range(self.num_layers):
+            s = _Spec()
+            _check(_lib.kvt_config_layer(h, i, ctypes.byref(s)))
+            self.layers.append(LayerSpec(s.mode, s.key_bits, s.value_bits, s.group, s.residual))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _lib is not None:
+            _lib.kvt_config_free(h)
+            self._h = None
+
+
+def load_config(path_or_json: str) -> Config:
+    return Config(path_or_json)
+
+
+def validate_spec(spec: LayerSpec, head_dim: int = 128):
+    s = spec._c()
+    _check(_lib.kvt_validate_spec(ctypes.byref(s), head_dim))
+
+
+def cache_buffer_sizes(spec: LayerSpec, batch: int, kv_heads: int, head_dim: int, capacity: int):
+    out = (ctypes.c_uint64 * 6)()
+    s = spec._c()
+    _check(_lib.kvt_cache_buffer_sizes(ctypes.byref(s), batch, kv_heads, head_dim, capacity, out))
+    return [int(v) for v in out]
+
+
+BUFFER_NAMES = ("k_codes", "k_meta", "k_resid", "v_codes", "v_meta", "v_resid")
+
+
+class LayerCache:
+    """One layer's packed cache; the six buffers are torch uint8 tensors owned here."""
+
+    def __init__(self, spec: LayerSpec, batch: int, kv_heads: int, head_dim: int, capacity: int,
+                 device="cuda"):
+        self.spec, self.batch, self.kv_heads, self.head_dim, self.capacity = spec, batch, kv_heads, head_dim, capacity
+        sizes = cache_buffer_sizes(spec, batch, kv_heads, head_dim, capacity)
+        self.sizes = dict(zip(BUFFER_NAMES, sizes))
+        self.buffers = {n: (torch.empty(max(sz, 16), dtype=torch.uint8, device=device) if sz else None)
+                        for n, sz in self.sizes.items()}
+        self._c = _Cache(spec._c(), batch, kv_heads, head_dim, capacity,
+                         *[(b.data_ptr() if b is not None else None) for b in self.buffers.values()])
+
+    def slice_view(self, name: str, b: int, h: int) -> torch.Tensor:
+        """Bytes of buffer `name` for (batch row b, kv head h)."""
+        per = self.sizes[name] // (self.batch * self.kv_heads)
+        off = (b * self.kv_heads + h) * per
+        return self.buffers[name][off:off + per]
+
+    @property
+    def nbytes(self) -> int:
+        return sum(self.sizes.values())
+
+
+# ------------------------------------------------------------------------------------------------
+# a2/a3: quantise on append
+# ------------------------------------------------------------------------------------------------
+def quantize_append(cache: LayerCache, k_new: torch.Tensor, v_new: torch.Tensor, len_before: torch.Tensor,
+                    n_new: torch.Tensor, len_before_host=None, n_new_host=None, n_new_max: Optional[int] = None,
+                    stream=None):
+    """k_new/v_new: bf16 [B][H][T][d] (d contiguous); len_before/n_new: int32 [B] on the device."""
+    _dev(k_new, "k_new", torch.bfloat16)
+    _dev(v_new, "v_new", torch.bfloat16)
+    _dev(len_before, "len_before", torch.int32)
+    _dev(n_new, "n_new", torch.int32)
+    if k_new.shape != v_new.shape or k_new.stride() != v_new.stride() or k_new.stride(-1) != 1:
+        raise ValueError("k_new and v_new need the same shape/strides with a contiguous last dim")
+    strides = (ctypes.c_int64 * 3)(k_new.stride(0), k_new.stride(1), k_new.stride(2))
+    if n_new_max is None:
+        n_new_max = k_new.shape[2]
+    _check(_lib.kvt_quantize_append(ctypes.byref(cache._c), _ptr(k_new), _ptr(v_new), strides,
+                                    _host_i32(len_before_host), _ptr(len_before), _host_i32(n_new_host),
+                                    _ptr(n_new), int(n_new_max), ctypes.c_void_p(_stream(stream))))
+
+
+# ------------------------------------------------------------------------------------------------
+# a4/a5: decode attention
+# ------------------------------------------------------------------------------------------------
+def decode_workspace_bytes(cache: LayerCache, n_q_heads: int, seq_len_host=None) -> int:
+    out = ctypes.c_uint64()
+    _check(_lib.kvt_decode_workspace_bytes(ctypes.byref(cache._c), n_q_heads, _host_i32(seq_len_host),
+                                           ctypes.byref(out)))
+    return int(out.value)
+
+
+def decode_attention(cache: LayerCache, q: torch.Tensor, seq_len: torch.Tensor, seq_len_host=None,
+                     scale: Optional[float] = None, out: Optional[torch.Tensor] = None,
+                     out_dtype=torch.float32, workspace: Optional[torch.Tensor] = None, stream=None):
+    """q: bf16 [B][H_q][d]; seq_len: int32 [B] (device).  Returns out [B][H_q][d] (fp32 or bf16)."""
+    _dev(q, "q", torch.bfloat16)
+    _dev(seq_len, "seq_len", torch.int32)
+    q = q.contiguous()
+    B, H_q, d = q.shape
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)                          # A9
+    if out is None:
+        out = torch.empty(B, H_q, d, dtype=out_dtype, device=q.device)
+    od = 1 if out.dtype == torch.float32 else 0
+    if out.dtype not in (torch.float32, torch.bfloat16) or not out.is_contiguous():
+        raise ValueError("out must be a contiguous fp32 or bf16 tensor")
+    if workspace is None:
+        nb = decode_workspace_bytes(cache, H_q, seq_len_host)
+        workspace = torch.empty(max(nb, 16), dtype=torch.uint8, device=q.device)
+    _check(_lib.kvt_decode_attention(ctypes.byref(cache._c), _ptr(q), H_q, _host_i32(seq_len_host), _ptr(seq_len),
+                                     float(scale), _ptr(out), od, _ptr(workspace), workspace.numel(),
+                                     ctypes.c_void_p(_stream(stream))))
+    return out
+
+
+def decode_attention_partial(cache: LayerCache, q: torch.Tensor, seq_len: torch.Tensor, seq_len_host=None,
+                             scale: Optional[float] = None, partial: Optional[torch.Tensor] = None,
+                             workspace: Optional[torch.Tensor] = None, stream=None):
+    """Partial (m, l, o) fp32 [B][H_q][d + 2] over this shard's tokens (a6)."""
+    _dev(q, "q", torch.bfloat16)
+    q = q.contiguous()
+    B, H_q, d = q.shape
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)
+    if partial is None:
+        partial = torch.empty(B, H_q, d + 2, dtype=torch.float32, device=q.device)
+    if workspace is None:
+        nb = decode_workspace_bytes(cache, H_q, seq_len_host)
+        workspace = torch.empty(max(nb, 16), dtype=torch.uint8, device=q.device)
+    _check(_lib.kvt_decode_attention_partial(ctypes.byref(cache._c), _ptr(q), H_q, _host_i32(seq_len_host),
+                                             _ptr(seq_len), float(scale), _ptr(partial), _ptr(workspace),
+                                             workspace.numel(), ctypes.c_void_p(_stream(stream))))
+    return partial
+
+
+def combine_partials(gathered: torch.Tensor, out: Optional[torch.Tensor] = None, out_dtype=torch.float32,
+                     stream=None):
+    """gathered: fp32 [N][B][H_q][d + 2] → out [B][H_q][d]."""
+    _dev(gathered, "gathered", torch.float32)
+    gathered = gathered.contiguous()
+    N, B, H_q, d2 = gathered.shape
+    d = d2 - 2
+    if out is None:
+        out = torch.empty(B, H_q, d, dtype=out_dtype, device=gathered.device)
+    od = 1 if out.dtype == torch.float32 else 0
+    _check(_lib.kvt_combine_partials(_ptr(gathered), N, B, H_q, d, _ptr(out), od, ctypes.c_void_p(_stream(stream))))
+    return out
+
+
+# ------------------------------------------------------------------------------------------------
+# a7: layer sensitivity
+# ------------------------------------------------------------------------------------------------
+ERROR_NAMES = ("e_k", "e_v", "e_a", "e_o", "e_o_l1")
+
+
+def layer_sensitivity(mode: int, group: int, residual: int, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
+                      q_pos0: int, pairs: Sequence[tuple], scale: Optional[float] = None, stream=None):
+    """q bf16 [H_q][T_q][d]; k, v bf16 [H_kv][S][d] → fp64 [n_pairs][5] on the device."""
+    for t, n in ((q, "q"), (k, "k"), (v, "v")):
+        _dev(t, n, torch.bfloat16)
+    q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+    H_q, T_q, d = q.shape
+    H_kv, S, _ = k.shape
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)
+    cp = (_Pair * len(pairs))(*[_Pair(int(a), int(b)) for a, b in pairs])
+    nb = ctypes.c_uint64()
+    _check(_lib.kvt_sensitivity_workspace_bytes(H_q, T_q, H_kv, S, d, group, ctypes.byref(nb)))
+    ws = torch.empty(max(int(nb.value), 16), dtype=torch.uint8, device=q.device)
+    out = torch.empty(len(pairs), 5, dtype=torch.float64, device=q.device)
+    _check(_lib.kvt_layer_sensitivity(mode, group, residual, _ptr(q), H_q, T_q, q_pos0, _ptr(k), _ptr(v), H_kv, S,
+                                      d, float(scale), cp, len(pairs), _ptr(out), _ptr(ws), ws.numel(),
+                                      ctypes.c_void_p(_stream(stream))))
+    return out
