@@ -265,8 +265,8 @@ def run_kvt(args):
     q = [(0.5 * torch.randn(B, Hq, D, device=dev, generator=gen)).to(torch.bfloat16) for _ in range(L)]
     outs = [torch.empty(B, Hq, D, dtype=torch.bfloat16, device=dev) for _ in range(L)]
     ws_bytes = max(kvt.decode_workspace_bytes(c, Hq, [cap] * B) for c in caches)
-    ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=dev)
-    n_combine = sum(1 for c in caches if kvt.decode_workspace_bytes(c, Hq, [cap] * B) > 0)
+    ws = torch.zeros(max(ws_bytes, 16), dtype=torch.uint8, device=dev)      # split counters start at zero
+    n_combine = 0     # the tensor-core kernel merges its splits in-kernel (last CTA); see launches.csv
     len_before = torch.full((B,), S0, dtype=torch.int32, device=dev)
     len_after = torch.full((B,), S0 + 1, dtype=torch.int32, device=dev)
     ones = torch.ones(B, dtype=torch.int32, device=dev)

@@ -134,7 +134,9 @@ int32_t kvt_quantize_append(const kvt_layer_cache* cache, const void* k_new, con
  * (out_dtype 0, RNE of the fp32 result).  seq_len_dev: int32 [B] device; seq_len_host: optional
  * int32 [B] host copy for validation and split planning (NULL: plan for `capacity`).
  * softmax_scale is normally 1/sqrt(d) (A9).  A sequence of length 0 yields a zero row.
- * The split-KV partials live in `workspace` (size from kvt_decode_workspace_bytes). */
+ * The split-KV partials live in `workspace` (size from kvt_decode_workspace_bytes).  The workspace must
+ * be zero-filled before its first use (it holds per-(b, kv head) split-arrival counters); every call
+ * leaves those counters at zero again, so one workspace can be reused by consecutive calls on a stream. */
 int32_t kvt_decode_workspace_bytes(const kvt_layer_cache* cache, int32_t n_q_heads,
                                    const int32_t* seq_len_host, uint64_t* bytes);
 int32_t kvt_decode_attention(const kvt_layer_cache* cache, const void* q, int32_t n_q_heads,

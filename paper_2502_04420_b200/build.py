@@ -35,48 +35,53 @@ def headers():
     return sorted(list(CSRC.glob("*.h")) + list(CSRC.glob("*.cuh")) + list(INCLUDE.glob("*.h")))
 
 
-def _compile(src: Path, force: bool) -> tuple[Path, str]:
-    obj = BUILD / (src.name + ".o")
+def _compile(src: Path, force: bool, defines=(), bdir: Path = BUILD) -> tuple[Path, str]:
+    obj = bdir / (src.name + ".o")
     dep_mtime = max([src.stat().st_mtime] + [h.stat().st_mtime for h in headers()])
     if not force and obj.exists() and obj.stat().st_mtime >= dep_mtime:
         return obj, ""
     lang = ["-x", "cu"]
-    cmd = [NVCC, *ARCH, *CFLAGS, *lang, "-c", str(src), "-o", str(obj)]
+    cmd = [NVCC, *ARCH, *CFLAGS, *[f"-D{d}" for d in defines], *lang, "-c", str(src), "-o", str(obj)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src.name}:\n{r.stdout}\n{r.stderr}")
     return obj, r.stderr
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    BUILD.mkdir(exist_ok=True)
+def build(force: bool = False, verbose: bool = False, defines=(), variant: str = "") -> Path:
+    """Build libkvt.so (or, for kernel A/B experiments, libkvt_<variant>.so with extra -D defines)."""
+    bdir = BUILD / variant if variant else BUILD
+    lib = LIB.with_name(f"libkvt_{variant}.so") if variant else LIB
+    bdir.mkdir(parents=True, exist_ok=True)
     srcs = sources()
     with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as ex:
-        results = list(ex.map(lambda s: _compile(s, force), srcs))
+        results = list(ex.map(lambda s: _compile(s, force, defines, bdir), srcs))
     logs = [log for _, log in results if log]
     if logs:
-        (BUILD / "ptxas.log").write_text("\n".join(logs))
+        (bdir / "ptxas.log").write_text("\n".join(logs))
     objs = [o for o, _ in results]
     newest = max(o.stat().st_mtime for o in objs)
-    if force or not LIB.exists() or LIB.stat().st_mtime < newest:
-        tmp = LIB.with_name(f"libkvt.so.tmp{os.getpid()}")
+    if force or not lib.exists() or lib.stat().st_mtime < newest:
+        tmp = lib.with_name(f"{lib.name}.tmp{os.getpid()}")
         cmd = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-cudart", "static", "-o", str(tmp), *map(str, objs)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-        os.replace(tmp, LIB)
+        os.replace(tmp, lib)
     if verbose:
-        print(f"built {LIB}")
-    return LIB
+        print(f"built {lib}")
+    return lib
 
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--variant", default="")
+    ap.add_argument("-D", dest="defines", action="append", default=[])
     a = ap.parse_args()
     try:
-        build(a.force, a.verbose or True)
+        build(a.force, a.verbose or True, a.defines, a.variant)
     except RuntimeError as e:
         print(e, file=sys.stderr)
         sys.exit(1)

@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <mutex>
 
 #include "kvt_decode.cuh"
@@ -13,6 +14,9 @@ KFn get_decode_k2(int VB, bool KPC, int GM);
 KFn get_decode_k4(int VB, bool KPC, int GM);
 KFn get_decode_k8(int VB, bool KPC, int GM);
 KFn get_decode_k16(int VB, bool KPC, int GM);
+KFn get_decode_mma_k2(int VB, int GM, size_t* smem);
+KFn get_decode_mma_k4(int VB, int GM, size_t* smem);
+KFn get_decode_mma_k8(int VB, int GM, size_t* smem);
 
 // K3: merge n_parts partial rows [n_parts][rows][2 + D] -> out (bf16 / fp32 / partial).  One warp
 // per row; lane owns 4 channels.
@@ -70,28 +74,44 @@ struct Instance {
     int occ = 1;
 };
 
+// KVT_DECODE_GENERIC=1 forces the CUDA-core kernel everywhere (A/B testing of the two kernels).
+static bool dec_force_generic() {
+    static const bool v = [] { const char* e = getenv("KVT_DECODE_GENERIC"); return e && e[0] == '1'; }();
+    return v;
+}
+
 static int bits_index(int b) { return b == 2 ? 0 : b == 4 ? 1 : b == 8 ? 2 : 3; }
 
 // Per-device cache of (function, smem, occupancy) for each instance; configured once.
 static std::mutex g_mu;
-static Instance g_inst[8][4][4][2][2];   // [device][kb][vb][kpc][gm]
-static bool g_ready[8][4][4][2][2];
+static Instance g_inst[8][4][4][3][2];   // [device][kb][vb][kind: 0 generic per-token, 1 generic per-channel, 2 mma][gm]
+static bool g_ready[8][4][4][3][2];
 static int g_sms[8];
 
-static int32_t get_instance(int kb, int vb, bool kpc, int GM, Instance* out, int* sms) {
+// kind: 0 = generic CUDA-core kernel (per-token key), 1 = generic (per-channel key), 2 = tensor-core KIVI
+static int32_t get_instance(int kb, int vb, int kind, int GM, Instance* out, int* sms) {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 8) return fail(KVT_ERR_CUDA, "cudaGetDevice failed");
-    int ki = bits_index(kb), vi = bits_index(vb), pi = kpc ? 1 : 0, gi = GM == 4 ? 0 : 1;
+    int ki = bits_index(kb), vi = bits_index(vb), gi = GM == 4 ? 0 : 1;
     std::lock_guard<std::mutex> lk(g_mu);
-    if (!g_ready[dev][ki][vi][pi][gi]) {
+    if (!g_ready[dev][ki][vi][kind][gi]) {
         Instance in;
-        switch (kb) {
-            case 2: in.fn = get_decode_k2(vb, kpc, GM); break;
-            case 4: in.fn = get_decode_k4(vb, kpc, GM); break;
-            case 8: in.fn = get_decode_k8(vb, kpc, GM); break;
-            default: in.fn = get_decode_k16(vb, kpc, GM); break;
+        if (kind == 2) {
+            switch (kb) {
+                case 2: in.fn = get_decode_mma_k2(vb, GM, &in.smem); break;
+                case 4: in.fn = get_decode_mma_k4(vb, GM, &in.smem); break;
+                default: in.fn = get_decode_mma_k8(vb, GM, &in.smem); break;
+            }
+        } else {
+            const bool kpc = kind == 1;
+            switch (kb) {
+                case 2: in.fn = get_decode_k2(vb, kpc, GM); break;
+                case 4: in.fn = get_decode_k4(vb, kpc, GM); break;
+                case 8: in.fn = get_decode_k8(vb, kpc, GM); break;
+                default: in.fn = get_decode_k16(vb, kpc, GM); break;
+            }
+            in.smem = smem_bytes(vb, GM);
         }
-        in.smem = smem_bytes(vb, GM);
         cudaError_t e = cudaFuncSetAttribute(in.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)in.smem);
         if (e != cudaSuccess) return fail(KVT_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&in.occ, in.fn, kThreads, in.smem);
@@ -101,10 +121,10 @@ static int32_t get_instance(int kb, int vb, bool kpc, int GM, Instance* out, int
             cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
             g_sms[dev] = n > 0 ? n : 148;
         }
-        g_inst[dev][ki][vi][pi][gi] = in;
-        g_ready[dev][ki][vi][pi][gi] = true;
+        g_inst[dev][ki][vi][kind][gi] = in;
+        g_ready[dev][ki][vi][kind][gi] = true;
     }
-    *out = g_inst[dev][ki][vi][pi][gi];
+    *out = g_inst[dev][ki][vi][kind][gi];
     *sms = g_sms[dev];
     return KVT_OK;
 }
@@ -122,15 +142,25 @@ static int plan_splits(const Geometry& g, int plan_len, int occ, int sms) {
     return n;
 }
 
+// The tensor-core kernel covers KIVI layers with G = 32 and 2/4/8-bit K and V; everything else runs
+// the generic CUDA-core kernel.
+static int kernel_kind(const Geometry& g) {
+    if (g.key_per_channel && g.G == 32 && g.kb != 16 && g.vb != 16 && !dec_force_generic()) return 2;
+    return g.key_per_channel ? 1 : 0;
+}
+
 }  // namespace dec
+
+static size_t parts_bytes(int ns, int B, int H_q) { return ((size_t)ns * B * H_q * (dec::D + 2) * sizeof(float) + 255) & ~(size_t)255; }
+static size_t counters_bytes(const Geometry& g) { return ((size_t)g.B * g.H * sizeof(int) + 255) & ~(size_t)255; }
 
 size_t decode_workspace(const Geometry& g, int H_q, int plan_len) {
     using namespace dec;
     int GM = (H_q / g.H) <= 4 ? 4 : 8;
     Instance in; int sms = 148;
-    if (get_instance(g.kb, g.vb, g.key_per_channel, GM, &in, &sms) != KVT_OK) { in.occ = 4; sms = 148; }
+    if (get_instance(g.kb, g.vb, kernel_kind(g), GM, &in, &sms) != KVT_OK) { in.occ = 4; sms = 148; }
     int ns = plan_splits(g, plan_len, in.occ, sms);
-    return ns > 1 ? (size_t)ns * g.B * H_q * (D + 2) * sizeof(float) : 0;
+    return ns > 1 ? parts_bytes(ns, g.B, H_q) + counters_bytes(g) : 0;
 }
 
 int32_t launch_decode(const Geometry& g, const CachePtrs& c, const uint16_t* q, int H_q, const int32_t* seq_len,
@@ -140,10 +170,11 @@ int32_t launch_decode(const Geometry& g, const CachePtrs& c, const uint16_t* q, 
     const int gq = H_q / g.H;
     const int GM = gq <= 4 ? 4 : 8;
     Instance in; int sms = 148;
-    int32_t st = get_instance(g.kb, g.vb, g.key_per_channel, GM, &in, &sms);
+    int32_t st = get_instance(g.kb, g.vb, kernel_kind(g), GM, &in, &sms);
     if (st) return st;
     int ns = plan_splits(g, plan_len, in.occ, sms);
-    size_t need = ns > 1 ? (size_t)ns * g.B * H_q * (D + 2) * sizeof(float) : 0;
+    const int kind = kernel_kind(g);
+    size_t need = ns > 1 ? parts_bytes(ns, g.B, H_q) + counters_bytes(g) : 0;
     if (need > ws_bytes || (need && !workspace))
         return fail(KVT_ERR_WORKSPACE, "decode: workspace %zu < %zu bytes (use kvt_decode_workspace_bytes)", ws_bytes, need);
     if (g.B > 65535 || g.H > 65535) return fail(KVT_ERR_UNSUPPORTED, "decode: batch/heads exceed grid limits");
@@ -154,11 +185,16 @@ int32_t launch_decode(const Geometry& g, const CachePtrs& c, const uint16_t* q, 
     a.out_mode = ns > 1 ? 3 : out_mode;
     a.parts = (float*)workspace;
     a.n_split = ns;
+    // tensor-core kernel: the last CTA per (b, kv head) merges the splits (workspace counters, zero between
+    // calls); the generic kernel uses the separate combine launch
+    const bool fused = (ns > 1) && (kind == 2);
+    a.counters = fused ? (int*)((char*)workspace + parts_bytes(ns, g.B, H_q)) : nullptr;
+    a.final_mode = out_mode;
     dim3 grid(ns, g.H, g.B);
     in.fn<<<grid, kThreads, in.smem, (cudaStream_t)stream>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(KVT_ERR_CUDA, "decode launch: %s", cudaGetErrorString(e));
-    if (ns > 1) {
+    if (ns > 1 && !fused) {
         int rows = g.B * H_q;
         combine_kernel<<<(rows + 3) / 4, 128, 0, (cudaStream_t)stream>>>((const float*)workspace, ns, rows, out, out_mode);
         e = cudaGetLastError();

@@ -52,6 +52,8 @@ struct DecodeArgs {
     int out_mode;      // 0 final bf16, 1 final fp32, 2 partial (m, l, o) -> out; 3 -> parts (split)
     float* parts;      // [n_split][B][H_q][D + 2] when out_mode == 3
     int n_split;
+    int* counters;     // [B][H_kv] split-arrival counters (fused combine), zero between calls; or null
+    int final_mode;    // output mode of the fused combine (0, 1 or 2)
 };
 
 __device__ __forceinline__ float bf2f(uint32_t b16) { return __uint_as_float(b16 << 16); }

@@ -1,5 +1,6 @@
 // Instances of the decode kernel for key bits = 4 (split across files for parallel compilation).
 #include "kvt_decode.cuh"
+#include "kvt_decode_mma.cuh"
 
 namespace kvt {
 namespace dec {
@@ -23,6 +24,15 @@ static KFn pick_vb(int VB, int GM) {
 
 KFn get_decode_k4(int VB, bool KPC, int GM) {
     return KPC ? pick_vb<true>(VB, GM) : pick_vb<false>(VB, GM);
+}
+
+// tensor-core KIVI instances (G = 32): returns the kernel and its dynamic shared memory
+KFn get_decode_mma_k4(int VB, int GM, size_t* smem) {
+    switch (VB) {
+        case 2: *smem = mma::Geo<4, 2>::SMEM; return GM == 4 ? mma::decode_mma_kernel<4, 2, 4> : mma::decode_mma_kernel<4, 2, 8>;
+        case 4: *smem = mma::Geo<4, 4>::SMEM; return GM == 4 ? mma::decode_mma_kernel<4, 4, 4> : mma::decode_mma_kernel<4, 4, 8>;
+        default: *smem = mma::Geo<4, 8>::SMEM; return GM == 4 ? mma::decode_mma_kernel<4, 8, 4> : mma::decode_mma_kernel<4, 8, 8>;
+    }
 }
 
 }  // namespace dec

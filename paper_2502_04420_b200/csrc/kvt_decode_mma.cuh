@@ -1,0 +1,741 @@
+// kvt_decode_mma.cuh — K2 fast path: KIVI decode attention with both dot products on the tensor
+// cores (mma.sync m16n8k16, fp16 operands, fp32 accumulation) — DESIGN.md §5.
+//
+// Why tensor cores on an HBM-bound kernel: with GQA (g = 4..8 query heads per KV head) and 2..4-bit
+// codes the CUDA-core form needs ~1k lane-instructions per (token, KV head) (2·g·d FMAs plus code
+// conversion) and ncu showed it issue-limited far below the HBM roofline.  Here the FMAs become
+// 1-2 HMMA per 16 tokens; what remains per code is about one LOP3.
+//
+// Operands (all products exact, fp32 accumulation):
+//   * A = the integer codes as fp16 *subnormals*: (word & mask) read as a half is code · 2^(p-24)
+//     where p is the bit position of the code inside its 16-bit half; no conversion instruction is
+//     needed.  The 2^(p-24) is undone exactly: per k-slot in B (QK) or per output row (PV).
+//   * B (QK) = q·s (the KIVI per-channel key scale of the block) times powers of two, split
+//     exactly into fp16 hi + lo (q and s are bf16 = 8 significant bits, so q·s has <= 16 bits); with
+//     g <= 4 the hi and lo halves share one N = 8 MMA.
+//   * B (PV) = p·s_v (probability times the per-token value scale) in fp16 times a power of two that
+//     only decreases along the sequence: relative rounding 2^-12 per weight.
+//   * zero-points in fp32: bias_h = sum_c q_c z_c per key block, sum_t p_t z_(t,group) per value group.
+//
+// One warp owns whole 32-token tiles (= KIVI key blocks, G = 32) fed by its own cp.async ring (K codes,
+// K block meta, V codes with padded rows, V meta).  Thread (gid = lane/4, tig = lane%4):
+//   QK  m-tile = 16 tokens (rows gid, gid+8), n = 8 (heads, or 4 heads x {hi, lo}), k = 16 channels;
+//       thread tig owns the 32-channel block [32 tig, 32 tig + 32) of each row (one LDS.128 at 4 bits).
+//   PV  m-tile = 16 channels of ONE value group γ (so the per-token value scale folds into B), n = 8
+//       heads, k = 16 tokens ordered in pairs (T, T+8); thread gid owns channels 32γ + 4gid + {0..3}.
+#pragma once
+#include <cuda_fp16.h>
+
+#include "kvt_decode.cuh"
+
+namespace kvt {
+namespace mma {
+
+using dec::DecodeArgs;
+using dec::Slice;
+using dec::bf2f;
+using dec::kFull;
+constexpr int D = 128;
+constexpr int kTile = 32;
+constexpr int kWarps = 4;
+constexpr int kThreads = 128;
+
+__device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+__device__ __forceinline__ __half2 u2h(uint32_t u) { return *reinterpret_cast<__half2*>(&u); }
+
+__device__ __forceinline__ void hmma(float d[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                     uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};\n"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// x >> 8 and x0 | x1 << 16 computed on the FMA pipe (IMAD.HI / IMAD) instead of the ALU pipe, which the
+// code extraction (LOP3) already saturates: the constants are made opaque so ptxas keeps the multiplies.
+// The two multipliers live in registers loaded once per thread (opaque to the optimiser).
+struct Mul { uint32_t k24, k16; };
+__device__ __forceinline__ Mul make_mul() {
+    Mul m;
+    asm volatile("mov.b32 %0, 0x01000000;" : "=r"(m.k24));
+    asm volatile("mov.b32 %0, 0x00010000;" : "=r"(m.k16));
+    return m;
+}
+#ifndef KVT_FMA_SHIFT
+#define KVT_FMA_SHIFT 0
+#endif
+#ifndef KVT_NEGF
+#define KVT_NEGF 0
+#endif
+#ifndef KVT_MINB
+#define KVT_MINB 4
+#endif
+__device__ __forceinline__ uint32_t shr8(uint32_t x, const Mul& k) {
+#if KVT_FMA_SHIFT
+    uint32_t r;
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(k.k24));
+    return r;
+#else
+    return x >> 8;
+#endif
+}
+__device__ __forceinline__ uint32_t pack16(uint32_t lo, uint32_t hi, const Mul& k) {   // lo, hi < 2^16
+#if KVT_FMA_SHIFT
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(hi), "r"(k.k16), "r"(lo));
+    return r;
+#else
+    return __byte_perm(lo, hi, 0x5410);
+#endif
+}
+
+__device__ __forceinline__ int frexp_e(float x) {           // x = f 2^e, f in [0.5, 1); clamped
+    const int e = x > 0.0f ? (int)((__float_as_uint(x) >> 23) & 0xFF) - 126 : 0;
+    return e < -90 ? -90 : (e > 90 ? 90 : e);
+}
+__device__ __forceinline__ float pow2(int e) { return __uint_as_float((uint32_t)(127 + e) << 23); }
+
+// ---- QK A operand: thread tig's 32-channel key block -> 16 fp16-subnormal pairs ("slots") ----------
+// Slot m holds channels (c0(m), c1(m)) of the block at bit position P(m) inside each half; k-step s of
+// the MMA uses slots 2s (A columns 2tig, 2tig+1) and 2s+1 (A columns 2tig+8, 2tig+9).
+template <int KB>
+struct KSlots {
+    __host__ __device__ static constexpr int c0(int m) {
+        return KB == 4 ? 8 * (m >> 2) + (m & 3)
+                       : (KB == 2 ? 16 * (m >> 3) + ((m & 7) < 4 ? 0 : 4) + (m & 3) : 4 * (m >> 1) + 2 * (m & 1));
+    }
+    __host__ __device__ static constexpr int c1(int m) { return c0(m) + (KB == 4 ? 4 : (KB == 2 ? 8 : 1)); }
+    __host__ __device__ static constexpr int P(int m) { return KB == 4 ? 4 * (m & 1) : (KB == 2 ? 2 * (m & 3) : 0); }
+};
+
+template <int KB>
+__device__ __forceinline__ uint32_t k_slot(const uint32_t* w, int m, const Mul& km) {
+    if constexpr (KB == 4) {
+        const uint32_t src = (m & 2) ? shr8(w[m >> 2], km) : w[m >> 2];
+        return src & ((m & 1) ? 0x00F000F0u : 0x000F000Fu);
+    } else if constexpr (KB == 2) {
+        const uint32_t src = (m & 4) ? shr8(w[m >> 3], km) : w[m >> 3];
+        return src & (0x00030003u << (2 * (m & 3)));
+    } else {
+        return __byte_perm(w[m >> 1], 0u, (m & 1) ? 0x4342 : 0x4140);
+    }
+}
+
+// Inverse of KSlots: channel offset cc in [0, 32) -> slot * 2 + half
+template <int KB>
+__device__ __forceinline__ int k_slot_of(int cc) {
+    if constexpr (KB == 4) {
+        const int w = cc >> 3, i = cc & 7;
+        return ((4 * w + (i & 3)) << 1) | (i >> 2);
+    } else if constexpr (KB == 2) {
+        const int w = cc >> 4, i = cc & 15;
+        return ((8 * w + 4 * ((i >> 2) & 1) + (i & 3)) << 1) | (i >> 3);
+    } else {
+        const int w = cc >> 2, i = cc & 3;
+        return ((2 * w + (i >> 1)) << 1) | (i & 1);
+    }
+}
+
+// ---- PV A operand: channels 32γ + 4gid + e (e < 4) of tokens (T, T+8) -> 4 subnormal pairs ----------
+// h[e] = (code(T, e), code(T+8, e)) · 2^(VP(e) - 24)
+template <int VB>
+__host__ __device__ constexpr int VP(int e) { return VB == 4 ? 4 * (e & 1) : (VB == 2 ? 2 * e : 0); }
+
+template <int VB>
+__device__ __forceinline__ void v_pairs(const uint8_t* r0, const uint8_t* r1, int gamma, int gid, uint32_t h[4],
+                                        const Mul& km) {
+    if constexpr (VB == 4) {
+        const uint32_t x0 = *reinterpret_cast<const uint16_t*>(r0 + 16 * gamma + 2 * gid);
+        const uint32_t x1 = *reinterpret_cast<const uint16_t*>(r1 + 16 * gamma + 2 * gid);
+        const uint32_t y = pack16(x0, x1, km), y8 = shr8(y, km);
+        h[0] = y & 0x000F000Fu;
+        h[1] = y & 0x00F000F0u;
+        h[2] = y8 & 0x000F000Fu;
+        h[3] = y8 & 0x00F000F0u;
+    } else if constexpr (VB == 2) {
+        const uint32_t x0 = r0[8 * gamma + gid];
+        const uint32_t x1 = r1[8 * gamma + gid];
+        const uint32_t y = pack16(x0, x1, km);             // [x0.b0, 0, x1.b0, 0]
+        h[0] = y & 0x00030003u;
+        h[1] = y & 0x000C000Cu;
+        h[2] = y & 0x00300030u;
+        h[3] = y & 0x00C000C0u;
+    } else {
+        const uint32_t x0 = *reinterpret_cast<const uint32_t*>(r0 + 32 * gamma + 4 * gid);
+        const uint32_t x1 = *reinterpret_cast<const uint32_t*>(r1 + 32 * gamma + 4 * gid);
+        const uint32_t p01 = __byte_perm(x0, x1, 0x5140), p23 = __byte_perm(x0, x1, 0x7362);
+        h[0] = __byte_perm(p01, 0u, 0x4140);
+        h[1] = __byte_perm(p01, 0u, 0x4342);
+        h[2] = __byte_perm(p23, 0u, 0x4140);
+        h[3] = __byte_perm(p23, 0u, 0x4342);
+    }
+}
+
+// Output row writer: mode 0 bf16, 1 fp32 (o = O / L), 2 partial (m, l, o).
+__device__ __forceinline__ void write_row(void* out, int mode, size_t row, int c, float M, float L, float O) {
+    const float ov = L > 0.0f ? __fdiv_rn(O, L) : 0.0f;
+    if (mode == 2) {
+        float* pr = reinterpret_cast<float*>(out) + row * (2 + D);
+        if (c == 0) { pr[0] = M; pr[1] = L; }
+        pr[2 + c] = ov;
+    } else if (mode == 1) {
+        reinterpret_cast<float*>(out)[row * D + c] = ov;
+    } else {
+        reinterpret_cast<__nv_bfloat16*>(out)[row * D + c] = __float2bfloat16_rn(ov);
+    }
+}
+
+template <int KB, int VB>
+struct Geo {
+    static constexpr int KROW = 16 * KB;                 // bytes per key code row
+    static constexpr int VROW = 16 * VB;
+    static constexpr int VSTR = VROW + (VB == 8 ? 32 : 16);   // padded value row (conflict-free PV loads)
+    static constexpr int K_OFF = 0;
+    static constexpr int KM_OFF = K_OFF + kTile * KROW;
+    static constexpr int V_OFF = KM_OFF + D * 4;
+    static constexpr int VM_OFF = V_OFF + kTile * VSTR;
+    static constexpr int STAGE = VM_OFF + kTile * 16;
+    static constexpr int NS = 2;                         // double buffer: a tile takes ~3k cycles, far above DRAM latency
+    // per warp: ring + PV weight tile (half2 [4 γ][2 ks][8 pairs][8 heads]) + key scale slots (half2 [4][16])
+    static constexpr int W_OFF = NS * STAGE;
+    static constexpr int W_BYTES = 4 * 2 * 8 * 8 * 4;
+    static constexpr int SH_OFF = W_OFF + W_BYTES;
+    static constexpr int WARP_BYTES = SH_OFF + 4 * 16 * 4;
+    static constexpr int Q_BYTES = 8 * D * 4;            // q fp32 [8][128]
+    static constexpr int COMB_BYTES = 2 * kWarps * 8 * (2 + D) * 4;
+    static constexpr int BODY = kWarps * WARP_BYTES > COMB_BYTES ? kWarps * WARP_BYTES : COMB_BYTES;
+    static constexpr size_t SMEM = (size_t)Q_BYTES + BODY;
+};
+
+__device__ __forceinline__ void cp16(void* s, const void* g) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(s);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(g));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// GM: 4 (g <= 4: n = 4 heads x {hi, lo}) or 8 (g <= 8: separate hi and lo MMAs).
+template <int KB, int VB, int GM>
+__global__ void __launch_bounds__(kThreads, KVT_MINB) decode_mma_kernel(DecodeArgs a) {
+    using Gm = Geo<KB, VB>;
+    extern __shared__ __align__(16) uint8_t smem[];
+    float* q_s = reinterpret_cast<float*>(smem);                           // [8][128]
+    uint8_t* body = smem + Gm::Q_BYTES;
+    const Geometry& g = a.g;
+    const int split = blockIdx.x, hk = blockIdx.y, b = blockIdx.z;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int gid = lane >> 2, tig = lane & 3;
+    const int gq = a.gq;
+    const int S = a.seq_len[b];
+
+    uint8_t* wbase = body + warp * Gm::WARP_BYTES;
+    uint32_t* w_s = reinterpret_cast<uint32_t*>(wbase + Gm::W_OFF);        // half2 [4][2][8][8]
+    uint32_t* sh_s = reinterpret_cast<uint32_t*>(wbase + Gm::SH_OFF);      // half2 [4 tig][16 slots]
+
+    {   // q -> shared fp32 (zero for padded heads)
+        const uint16_t* qg = a.q + ((size_t)b * a.H_q + (size_t)hk * gq) * D;
+        for (int h = 0; h < 8; ++h) q_s[h * D + tid] = (h < gq && h < GM) ? bf2f(qg[(size_t)h * D + tid]) : 0.0f;
+    }
+    for (int i = lane; i < Gm::W_BYTES / 4; i += 32) w_s[i] = 0u;
+    __syncthreads();
+
+    const size_t bh = (size_t)b * g.H + hk;
+    Slice sl;
+    sl.kc = a.c.k_codes + bh * g.kc;
+    sl.km = a.c.k_meta + bh * (g.km / 4);
+    sl.kr = a.c.k_resid + bh * (g.kr / 2);
+    sl.vc = a.c.v_codes + bh * g.vc;
+    sl.vm = a.c.v_meta + bh * (g.vm / 4);
+    sl.vr = g.vr ? a.c.v_resid + bh * (g.vr / 2) : nullptr;
+
+    const int nqK = nq_key(g.mode, g.kb, g.G, g.R, S);
+    const int nqV = nq_per_token(g.vb, g.R, S);
+    const int n_main = ((nqK < nqV ? nqK : nqV) / kTile) * kTile;
+    const int n_tiles = n_main / kTile;
+    const int tps = (n_tiles + a.n_split - 1) / a.n_split;
+    const int tile_lo = split * tps;
+    const int tile_hi = (tile_lo + tps < n_tiles) ? tile_lo + tps : n_tiles;
+    const int n_my = tile_hi - tile_lo - warp > 0 ? (tile_hi - tile_lo - warp + kWarps - 1) / kWarps : 0;
+
+    // softmax heads of this thread (the QK D columns it holds after the hi/lo fold)
+    const int hA = (GM == 8) ? 2 * tig : 2 * (tig & 1);
+    // ---- per-head power-of-two scale of q (max |q 2^qa| in [64, 128)), computed once per CTA ----
+    float* qmax_s = reinterpret_cast<float*>(body) + 0;   // body is free until the ring is first used
+    if (warp == 0) {
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+            const float4 v = *reinterpret_cast<const float4*>(q_s + h * D + 4 * lane);
+            float m = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) m = fmaxf(m, __shfl_xor_sync(kFull, m, off));
+            if (lane == 0) qmax_s[h] = m;
+        }
+    }
+    __syncthreads();
+    uint32_t q_h[16];
+    float qa_inv[2];
+    {
+        const int qh = (GM == 4) ? (gid & 3) : gid;
+        const int qa = 7 - frexp_e(qmax_s[qh]);
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+            const float sc = pow2(qa - KSlots<KB>::P(m));
+            q_h[m] = h2u(__floats2half2_rn(q_s[qh * D + 32 * tig + KSlots<KB>::c0(m)] * sc,
+                                           q_s[qh * D + 32 * tig + KSlots<KB>::c1(m)] * sc));
+        }
+#pragma unroll
+        for (int j = 0; j < 2; ++j) qa_inv[j] = pow2(24 - (7 - frexp_e(qmax_s[hA + j])));   // undoes 2^qa, 2^-24
+    }
+    __syncthreads();
+    // GM == 4: lanes tig and tig^2 hold the same probabilities, so they prepare different value groups:
+    // relative group r (0, 1) of this lane is group 2 * (tig >> 1) + r.
+    const int gsh = (GM == 4) ? 2 * (tig >> 1) : 0;
+    const Mul kmul = make_mul();
+    constexpr int NGL = (GM == 4) ? 2 : 4;               // value groups prepared per lane
+
+    // ---- running state ----
+    float m_run[2] = {-INFINITY, -INFINITY};              // reference max (lazy: moves only by > 8)
+    float l_part[2] = {0.0f, 0.0f};
+    float zacc[4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) zacc[i][0] = zacc[i][1] = 0.0f;
+    float o[8][4];                 // PV accumulators: m-tile (γ, μ) = 2γ + μ
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.0f;
+    int kp = 126;                  // PV weight exponent (only decreases)
+
+    auto issue = [&](int it, int st) {
+        const int t0 = (tile_lo + warp + it * kWarps) * kTile;
+        uint8_t* sb = wbase + st * Gm::STAGE;
+        const uint8_t* gk = sl.kc + (size_t)t0 * Gm::KROW;
+#pragma unroll
+        for (int c = lane; c < kTile * Gm::KROW / 16; c += 32) cp16(sb + Gm::K_OFF + 16 * c, gk + 16 * c);
+        cp16(sb + Gm::KM_OFF + 16 * lane, reinterpret_cast<const uint8_t*>(sl.km + (size_t)(t0 / kTile) * D) + 16 * lane);
+        const uint8_t* gv = sl.vc + (size_t)t0 * Gm::VROW;
+#pragma unroll
+        for (int c = lane; c < kTile * Gm::VROW / 16; c += 32) {
+            const int row = c / (Gm::VROW / 16), col = c % (Gm::VROW / 16);
+            cp16(sb + Gm::V_OFF + row * Gm::VSTR + 16 * col, gv + 16 * c);
+        }
+        cp16(sb + Gm::VM_OFF + 16 * lane, reinterpret_cast<const uint8_t*>(sl.vm + (size_t)t0 * 4) + 16 * lane);
+    };
+
+#pragma unroll
+    for (int s = 0; s < Gm::NS - 1; ++s) {
+        if (s < n_my) issue(s, s);
+        cp_commit();
+    }
+    for (int it = 0; it < n_my; ++it) {
+        {
+            const int nx = it + Gm::NS - 1;
+            if (nx < n_my) issue(nx, nx % Gm::NS);
+            cp_commit();
+        }
+        cp_wait<Gm::NS - 1>();
+        __syncwarp();
+        const uint8_t* sb = wbase + (it % Gm::NS) * Gm::STAGE;
+        const uint8_t* kc_s = sb + Gm::K_OFF;
+        const uint32_t* km_s = reinterpret_cast<const uint32_t*>(sb + Gm::KM_OFF);
+        const uint8_t* vc_s = sb + Gm::V_OFF;
+        const uint32_t* vm_s = reinterpret_cast<const uint32_t*>(sb + Gm::VM_OFF);
+
+        // (1) key block meta: scale slots (fp16 x 2^sb) and the zero-point bias sum_c q_c z_c
+        float bias[2];
+        float ks_inv;
+        {
+            const uint4 m4 = reinterpret_cast<const uint4*>(km_s)[lane];
+            const uint32_t mw[4] = {m4.x, m4.y, m4.z, m4.w};
+            // the largest scale: positive bf16 bit patterns order like their values
+            uint32_t smb = max(max(mw[0] & 0xffffu, mw[1] & 0xffffu), max(mw[2] & 0xffffu, mw[3] & 0xffffu));
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) smb = max(smb, __shfl_xor_sync(kFull, smb, off));
+            const int sbx = 7 - frexp_e(bf2f(smb));
+            const float ssc = pow2(sbx);
+            ks_inv = pow2(-sbx);
+            __half* shh = reinterpret_cast<__half*>(sh_s);
+            float z[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int c = 4 * lane + e;
+                const int code = k_slot_of<KB>(c & 31);
+                shh[((c >> 5) * 16 + (code >> 1)) * 2 + (code & 1)] = __float2half_rn(bf2f(mw[e] & 0xffffu) * ssc);
+                z[e] = bf2f(mw[e] >> 16);
+            }
+            // bias partials of the GM heads, reduce-scattered: lane l ends with head (l & 7)
+            float bz[8];
+#pragma unroll
+            for (int h = 0; h < 8; ++h) {
+                if (h < GM) {
+                    const float4 qv = *reinterpret_cast<const float4*>(q_s + h * D + 4 * lane);
+                    bz[h] = qv.x * z[0] + qv.y * z[1] + qv.z * z[2] + qv.w * z[3];
+                } else {
+                    bz[h] = 0.0f;
+                }
+            }
+            {
+                const bool up = (lane >> 2) & 1;
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    if (h + 4 >= GM && h >= GM) continue;
+                    const float recv = __shfl_xor_sync(kFull, up ? bz[h] : bz[h + 4], 4);
+                    bz[h] = (up ? bz[h + 4] : bz[h]) + recv;
+                }
+            }
+            {
+                const bool up = (lane >> 1) & 1;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const float recv = __shfl_xor_sync(kFull, up ? bz[h] : bz[h + 2], 2);
+                    bz[h] = (up ? bz[h + 2] : bz[h]) + recv;
+                }
+            }
+            {
+                const bool up = lane & 1;
+                const float recv = __shfl_xor_sync(kFull, up ? bz[0] : bz[1], 1);
+                bz[0] = (up ? bz[1] : bz[0]) + recv;
+            }
+            bz[0] += __shfl_xor_sync(kFull, bz[0], 8);
+            bz[0] += __shfl_xor_sync(kFull, bz[0], 16);
+            bias[0] = __shfl_sync(kFull, bz[0], hA);
+            bias[1] = __shfl_sync(kFull, bz[0], hA + 1);
+        }
+        __syncwarp();
+        // (2) B operand of QK: q_h * s_h split exactly into hi + lo
+        uint32_t bq[16], bq_lo[(GM == 8) ? 16 : 1];
+        {
+            const uint4* shv = reinterpret_cast<const uint4*>(sh_s + tig * 16);
+            // GM == 4: lanes gid >= 4 carry the lo halves: b = fma(q, s, -f * hi) with f = 1 (lo) or 0 (hi)
+            const __half2 negf = __float2half2_rn((GM == 4 && gid >= 4) ? -1.0f : 0.0f);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint4 s4 = shv[u];
+                const uint32_t sv[4] = {s4.x, s4.y, s4.z, s4.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int m = 4 * u + e;
+                    const __half2 hi = __hmul2(u2h(q_h[m]), u2h(sv[e]));
+                    if constexpr (GM == 8) {
+                        bq[m] = h2u(hi);
+                        bq_lo[m] = h2u(__hfma2(u2h(q_h[m]), u2h(sv[e]), __hneg2(hi)));
+                    } else {
+#if KVT_NEGF
+                        bq[m] = h2u(__hfma2(u2h(q_h[m]), u2h(sv[e]), __hmul2(hi, negf)));
+#else
+                        bq[m] = (gid >= 4) ? h2u(__hfma2(u2h(q_h[m]), u2h(sv[e]), __hneg2(hi))) : h2u(hi);
+#endif
+                    }
+                }
+            }
+        }
+        // (3) QK on the tensor cores: two m-tiles of 16 tokens, 4 independent accumulator chains
+        float dq[2][4];
+        {
+            uint32_t w[4][KB];        // rows gid, gid+8, 16+gid, 24+gid
+#pragma unroll
+            for (int rr = 0; rr < 4; ++rr) {
+                const uint8_t* r0 = kc_s + (8 * rr + gid) * Gm::KROW + tig * 4 * KB;
+                if constexpr (KB == 2) {
+                    const uint2 x = *reinterpret_cast<const uint2*>(r0);
+                    w[rr][0] = x.x; w[rr][1] = x.y;
+                } else {
+#pragma unroll
+                    for (int u = 0; u < KB / 4; ++u) {
+                        const uint4 x = reinterpret_cast<const uint4*>(r0)[u];
+                        w[rr][4 * u] = x.x; w[rr][4 * u + 1] = x.y; w[rr][4 * u + 2] = x.z; w[rr][4 * u + 3] = x.w;
+                    }
+                }
+            }
+            float de[2][4], dd[2][4];
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) de[mt][i] = dd[mt][i] = 0.0f;
+#pragma unroll
+            for (int s = 0; s < 8; ++s) {
+#pragma unroll
+                for (int mt = 0; mt < 2; ++mt) {
+                    float* acc = (s & 1) ? dd[mt] : de[mt];
+                    const uint32_t a0 = k_slot<KB>(w[2 * mt], 2 * s, kmul), a1 = k_slot<KB>(w[2 * mt + 1], 2 * s, kmul);
+                    const uint32_t a2 = k_slot<KB>(w[2 * mt], 2 * s + 1, kmul), a3 = k_slot<KB>(w[2 * mt + 1], 2 * s + 1, kmul);
+                    hmma(acc, a0, a1, a2, a3, bq[2 * s], bq[2 * s + 1]);
+                    if constexpr (GM == 8) hmma(acc, a0, a1, a2, a3, bq_lo[2 * s], bq_lo[2 * s + 1]);
+                }
+            }
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    dq[mt][i] = de[mt][i] + dd[mt][i];
+                    if constexpr (GM == 4) dq[mt][i] += __shfl_xor_sync(kFull, dq[mt][i], 2);
+                }
+        }
+        // (4) logits (log2 domain) for tokens {16mt + gid + 8r} x heads {hA, hA + 1}; online softmax with a
+        // lazy reference max: it only moves when the tile max exceeds it by more than 8 (so p <= 2^8)
+        float alpha[2], p[2][2][2];        // p[mt][r][j]
+        bool resc = false;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const float cs = a.scale_log2 * qa_inv[j] * ks_inv;
+            const float cb = a.scale_log2 * bias[j];
+            float l4[4];
+            l4[0] = fmaf(dq[0][j], cs, cb);
+            l4[1] = fmaf(dq[0][2 + j], cs, cb);
+            l4[2] = fmaf(dq[1][j], cs, cb);
+            l4[3] = fmaf(dq[1][2 + j], cs, cb);
+            float mx = fmaxf(fmaxf(l4[0], l4[1]), fmaxf(l4[2], l4[3]));
+            mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 4));
+            mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 8));
+            mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 16));
+            alpha[j] = 1.0f;
+            if (mx > m_run[j] + 8.0f) {
+                alpha[j] = exp2f(m_run[j] - mx);
+                m_run[j] = mx;
+                resc = true;
+            }
+            const float mr = m_run[j];
+            p[0][0][j] = exp2f(l4[0] - mr);
+            p[0][1][j] = exp2f(l4[1] - mr);
+            p[1][0][j] = exp2f(l4[2] - mr);
+            p[1][1][j] = exp2f(l4[3] - mr);
+            l_part[j] = l_part[j] * alpha[j] + ((p[0][0][j] + p[0][1][j]) + (p[1][0][j] + p[1][1][j]));
+        }
+        // (5) value weights w = p * s_v * 2^kp (fp16 pairs (T, T+8)) and zero sums p * z_v
+        float kfac = 1.0f;
+        {
+            // meta words of this lane's 4 tokens x its value groups (GM == 4: the tig pair splits the groups)
+            uint32_t mw[2][2][NGL];
+            uint32_t smb = 0;
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    const uint32_t* row = vm_s + (16 * mt + gid + 8 * r) * 4 + gsh;
+                    if constexpr (NGL == 4) {
+                        const uint4 m4 = *reinterpret_cast<const uint4*>(row);
+                        mw[mt][r][0] = m4.x; mw[mt][r][1] = m4.y; mw[mt][r][2 % NGL] = m4.z; mw[mt][r][3 % NGL] = m4.w;
+                    } else {
+                        const uint2 m2 = *reinterpret_cast<const uint2*>(row);
+                        mw[mt][r][0] = m2.x; mw[mt][r][1] = m2.y;
+                    }
+#pragma unroll
+                    for (int gr = 0; gr < NGL; ++gr) smb = max(smb, mw[mt][r][gr] & 0xffffu);
+                }
+            if constexpr (GM == 4) smb = max(smb, __shfl_xor_sync(kFull, smb, 2));
+            smb = max(smb, __shfl_xor_sync(kFull, smb, 4));
+            smb = max(smb, __shfl_xor_sync(kFull, smb, 8));
+            smb = max(smb, __shfl_xor_sync(kFull, smb, 16));
+            const int kt = 7 - frexp_e(bf2f(smb));
+            if (kt < kp) {
+                if (it > 0) { kfac = pow2(kt - kp); resc = true; }
+                kp = kt;
+            }
+            const float ksc = pow2(kp);
+            float2 pk[2][2];           // (p(T), p(T+8)) * 2^kp for heads j: pk[mt][j]
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                for (int j = 0; j < 2; ++j)
+                    pk[mt][j] = dec::fmul2(make_float2(p[mt][0][j], p[mt][1][j]), make_float2(ksc, ksc));
+#pragma unroll
+            for (int gr = 0; gr < NGL; ++gr) {
+                const int gam = gsh + gr;
+                float2 za = make_float2(zacc[gr][0], zacc[gr][1]);
+                if (resc) za = dec::fmul2(za, make_float2(alpha[0], alpha[1]));
+#pragma unroll
+                for (int mt = 0; mt < 2; ++mt) {
+                    const uint32_t w0 = mw[mt][0][gr], w1 = mw[mt][1][gr];
+                    const float2 sv = make_float2(bf2f(w0 & 0xffffu), bf2f(w1 & 0xffffu));
+                    uint2 wv;
+                    const float2 wa = dec::fmul2(pk[mt][0], sv), wb = dec::fmul2(pk[mt][1], sv);
+                    wv.x = h2u(__floats2half2_rn(wa.x, wa.y));
+                    wv.y = h2u(__floats2half2_rn(wb.x, wb.y));
+                    *reinterpret_cast<uint2*>(w_s + ((gam * 2 + mt) * 8 + gid) * 8 + hA) = wv;
+                    const float z0 = __uint_as_float(w0 & 0xffff0000u), z1 = __uint_as_float(w1 & 0xffff0000u);
+                    za = dec::ffma2(make_float2(p[mt][0][0], p[mt][0][1]), make_float2(z0, z0), za);
+                    za = dec::ffma2(make_float2(p[mt][1][0], p[mt][1][1]), make_float2(z1, z1), za);
+                }
+                zacc[gr][0] = za.x;
+                zacc[gr][1] = za.y;
+            }
+        }
+        __syncwarp();
+        // (6) PV on the tensor cores: 8 m-tiles (γ, μ) x 2 k-steps of 16 tokens
+        {
+            if (__any_sync(kFull, resc)) {
+                const float r0 = alpha[0] * kfac, r1 = alpha[1] * kfac;   // PV columns 2tig, 2tig+1
+#pragma unroll
+                for (int i = 0; i < 8; ++i) { o[i][0] *= r0; o[i][1] *= r1; o[i][2] *= r0; o[i][3] *= r1; }
+            }
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) {
+                const uint8_t* vr0 = vc_s + (16 * ks + tig) * Gm::VSTR;       // tokens T = 16ks + tig, T + 8
+                const uint8_t* vr1 = vr0 + 8 * Gm::VSTR;
+                const uint8_t* vr2 = vr0 + 4 * Gm::VSTR;                       // tokens T + 4, T + 12
+                const uint8_t* vr3 = vr2 + 8 * Gm::VSTR;
+#pragma unroll
+                for (int gam = 0; gam < 4; ++gam) {
+                    const uint32_t* wr = w_s + (gam * 2 + ks) * 64 + gid;
+                    const uint32_t b0 = wr[tig * 8], b1 = wr[(tig + 4) * 8];
+                    uint32_t hA4[4], hB4[4];
+                    v_pairs<VB>(vr0, vr1, gam, gid, hA4, kmul);
+                    v_pairs<VB>(vr2, vr3, gam, gid, hB4, kmul);
+                    hmma(o[2 * gam], hA4[0], hA4[1], hB4[0], hB4[1], b0, b1);
+                    hmma(o[2 * gam + 1], hA4[2], hA4[3], hB4[2], hB4[3], b0, b1);
+                }
+            }
+        }
+        __syncwarp();
+    }
+    cp_wait<0>();
+
+    // ---- warp epilogue: l over the 8 row-groups, zero sums, o = D * 2^(24 - P(row) - kp) + zacc ----
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        float l = (GM == 8 || tig < 2) ? l_part[j] : 0.0f;
+        l += __shfl_xor_sync(kFull, l, 4);
+        l += __shfl_xor_sync(kFull, l, 8);
+        l += __shfl_xor_sync(kFull, l, 16);
+        l_part[j] = l;
+#pragma unroll
+        for (int gam = 0; gam < 4; ++gam) {
+            float z = zacc[gam][j];
+            z += __shfl_xor_sync(kFull, z, 4);
+            z += __shfl_xor_sync(kFull, z, 8);
+            z += __shfl_xor_sync(kFull, z, 16);
+            zacc[gam][j] = z;
+        }
+    }
+    if constexpr (GM == 4) {   // tig 0/1 hold groups 0,1 of heads (0,1)/(2,3) in slots 0,1; tig 2/3 groups 2,3
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            zacc[2][j] = __shfl_xor_sync(kFull, zacc[0][j], 2);
+            zacc[3][j] = __shfl_xor_sync(kFull, zacc[1][j], 2);
+        }
+    }
+    __syncthreads();                                   // the per-warp areas become the combine area
+    float* comb = reinterpret_cast<float*>(body);      // [8 partials][8 heads][2 + D]
+    {
+        float* cw = comb + warp * 8 * (2 + D);
+        const bool owner = (GM == 8) || (tig < 2);     // PV columns 2tig, 2tig+1 are real heads
+        if (owner) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int h = 2 * tig + j;
+                float* ch = cw + h * (2 + D);
+                if (gid == 0) { ch[0] = m_run[j]; ch[1] = l_part[j]; }
+#pragma unroll
+                for (int gam = 0; gam < 4; ++gam)
+#pragma unroll
+                    for (int mu = 0; mu < 2; ++mu) {
+                        const int c = 32 * gam + 4 * gid + 2 * mu;
+                        ch[2 + c] = o[2 * gam + mu][j] * pow2(24 - VP<VB>(2 * mu) - kp) + zacc[gam][j];
+                        ch[2 + c + 1] = o[2 * gam + mu][2 + j] * pow2(24 - VP<VB>(2 * mu + 1) - kp) + zacc[gam][j];
+                    }
+            }
+        }
+    }
+    // ---- tail tokens [n_main, S) (last split): token at a time, lane = channels [4 lane, 4 lane + 4) ----
+    {
+        float* cw = comb + (kWarps + warp) * 8 * (2 + D);
+        float mt_[GM], lt[GM], ot[GM][4];
+#pragma unroll
+        for (int h = 0; h < GM; ++h) {
+            mt_[h] = -INFINITY; lt[h] = 0.0f;
+            ot[h][0] = ot[h][1] = ot[h][2] = ot[h][3] = 0.0f;
+        }
+        if (split == a.n_split - 1) {
+            for (int t = n_main + warp; t < S; t += kWarps) {
+                float kx[4], vx[4];
+                dec::tail_k<KB, true>(sl, g, t, nqK, lane, kx);
+                dec::tail_v<VB>(sl, g, t, nqV, lane, vx);
+#pragma unroll
+                for (int h = 0; h < GM; ++h) {
+                    const float4 qv = *reinterpret_cast<const float4*>(q_s + h * D + 4 * lane);
+                    float s = qv.x * kx[0] + qv.y * kx[1] + qv.z * kx[2] + qv.w * kx[3];
+#pragma unroll
+                    for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(kFull, s, off);
+                    s *= a.scale_log2;
+                    const float mn = fmaxf(mt_[h], s);
+                    const float al = exp2f(mt_[h] - mn);
+                    const float pp = exp2f(s - mn);
+                    lt[h] = lt[h] * al + pp;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) ot[h][i] = ot[h][i] * al + pp * vx[i];
+                    mt_[h] = mn;
+                }
+            }
+        }
+#pragma unroll
+        for (int h = 0; h < GM; ++h) {
+            float* ch = cw + h * (2 + D);
+            if (lane == 0) { ch[0] = mt_[h]; ch[1] = lt[h]; }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) ch[2 + 4 * lane + i] = ot[h][i];
+        }
+    }
+    __syncthreads();
+    // ---- CTA combine of the 8 partials: thread = channel ----
+    const int c = tid;
+    for (int h = 0; h < gq; ++h) {
+        float M = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < 2 * kWarps; ++w) M = fmaxf(M, comb[(w * 8 + h) * (2 + D)]);
+        float L = 0.0f, O = 0.0f;
+        if (M != -INFINITY) {
+#pragma unroll
+            for (int w = 0; w < 2 * kWarps; ++w) {
+                const float* cw = comb + (w * 8 + h) * (2 + D);
+                if (cw[1] == 0.0f) continue;
+                const float scl = exp2f(cw[0] - M);
+                L += cw[1] * scl;
+                O += cw[2 + c] * scl;
+            }
+        }
+        const size_t row = (size_t)b * a.H_q + (size_t)hk * gq + h;
+        if (a.out_mode == 3) {
+            float* pr = a.parts + ((size_t)split * g.B * a.H_q + row) * (2 + D);
+            if (c == 0) { pr[0] = M; pr[1] = L; }
+            pr[2 + c] = L > 0.0f ? __fdiv_rn(O, L) : 0.0f;
+        } else {
+            write_row(a.out, a.out_mode, row, c, M, L, O);
+        }
+    }
+    // ---- fused split combine (K3): the last CTA of this (b, kv head) to arrive merges the partials ----
+    if (a.out_mode == 3 && a.counters != nullptr) {
+        __shared__ int is_last;
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            const int old = atomicAdd(a.counters + bh, 1);
+            is_last = (old == a.n_split - 1);
+        }
+        __syncthreads();
+        if (is_last) {
+            __threadfence();
+            for (int h = 0; h < gq; ++h) {
+                const size_t row = (size_t)b * a.H_q + (size_t)hk * gq + h;
+                float M = -INFINITY;
+                for (int sp = 0; sp < a.n_split; ++sp)
+                    M = fmaxf(M, __ldcg(a.parts + ((size_t)sp * g.B * a.H_q + row) * (2 + D)));
+                float L = 0.0f, O = 0.0f;
+                if (M != -INFINITY) {
+                    for (int sp = 0; sp < a.n_split; ++sp) {
+                        const float* pr = a.parts + ((size_t)sp * g.B * a.H_q + row) * (2 + D);
+                        const float l = __ldcg(pr + 1);
+                        if (l == 0.0f) continue;
+                        const float wgt = l * exp2f(__ldcg(pr) - M);
+                        L += wgt;
+                        O += wgt * __ldcg(pr + 2 + c);
+                    }
+                }
+                write_row(a.out, a.final_mode, row, c, M, L, O);
+            }
+            if (tid == 0) a.counters[bh] = 0;
+        }
+    }
+}
+
+}  // namespace mma
+}  // namespace kvt

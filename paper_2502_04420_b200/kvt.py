@@ -15,7 +15,10 @@ from typing import Optional, Sequence
 
 import torch
 
-_LIB_PATH = Path(__file__).resolve().parent / "libkvt.so"
+import os
+
+# KVT_LIB selects an alternative build (kernel A/B experiments: libkvt_<variant>.so); default libkvt.so
+_LIB_PATH = Path(__file__).resolve().parent / os.environ.get("KVT_LIB", "libkvt.so")
 
 MODE_PER_TOKEN_ASYM = 0
 MODE_KIVI = 1
@@ -262,7 +265,7 @@ def decode_attention(cache: LayerCache, q: torch.Tensor, seq_len: torch.Tensor, 
         raise ValueError("out must be a contiguous fp32 or bf16 tensor")
     if workspace is None:
         nb = decode_workspace_bytes(cache, H_q, seq_len_host)
-        workspace = torch.empty(max(nb, 16), dtype=torch.uint8, device=q.device)
+        workspace = torch.zeros(max(nb, 16), dtype=torch.uint8, device=q.device)   # counters start at zero
     _check(_lib.kvt_decode_attention(ctypes.byref(cache._c), _ptr(q), H_q, _host_i32(seq_len_host), _ptr(seq_len),
                                      float(scale), _ptr(out), od, _ptr(workspace), workspace.numel(),
                                      ctypes.c_void_p(_stream(stream))))
@@ -282,7 +285,7 @@ def decode_attention_partial(cache: LayerCache, q: torch.Tensor, seq_len: torch.
         partial = torch.empty(B, H_q, d + 2, dtype=torch.float32, device=q.device)
     if workspace is None:
         nb = decode_workspace_bytes(cache, H_q, seq_len_host)
-        workspace = torch.empty(max(nb, 16), dtype=torch.uint8, device=q.device)
+        workspace = torch.zeros(max(nb, 16), dtype=torch.uint8, device=q.device)
     _check(_lib.kvt_decode_attention_partial(ctypes.byref(cache._c), _ptr(q), H_q, _host_i32(seq_len_host),
                                              _ptr(seq_len), float(scale), _ptr(partial), _ptr(workspace),
                                              workspace.numel(), ctypes.c_void_p(_stream(stream))))

@@ -34,6 +34,8 @@ def compare_slice(oracle, cache, spec, b, h, K_bits, V_bits, S, d=128):
     ref = oracle.build_cache(spec.mode, spec.key_bits, spec.value_bits, spec.group, spec.residual, d,
                              cache.capacity, K_bits, V_bits)
     for name, ranges in regions(oracle, spec, S, d).items():
+        if cache.buffers[name] is None or not any(hi > lo for lo, hi in ranges):
+            continue
         gpu = cache.slice_view(name, b, h).cpu().numpy().view(np.uint8)
         exp = ref[name].view(np.uint8)
         for lo, hi in ranges:

@@ -118,7 +118,7 @@ def test_decode_parity(kvt, oracle, name, mk, g):
     K = kvt_synth.keys((B, H, S_max, D), seed=301 + g).cuda()
     V = kvt_synth.values((B, H, S_max, D), seed=302 + g).cuda()
     q = kvt_synth.queries((B, H * g, D), seed=303 + g).cuda()
-    cap = ((S_max + 63) // 64) * 64
+    cap = ((S_max + 127) // 128) * 128
     cache = _prefill(kvt, spec, K, V, lens, cap)
     sl = torch.tensor(lens, dtype=torch.int32, device="cuda")
     scale = 1.0 / math.sqrt(D)
@@ -152,7 +152,15 @@ def test_decode_without_host_lengths(kvt, oracle):
     a = kvt.decode_attention(cache, q, sl, seq_len_host=lens)
     b = kvt.decode_attention(cache, q, sl, seq_len_host=None)
     torch.cuda.synchronize()
-    assert (a - b).abs().max().item() <= 1e-5 * a.abs().max().item()
+    # a different split plan changes only the fp32/fp16 rounding order (tile-local weight scaling)
+    Kb, Vb, qb = kvt_synth.bf16_bits(K), kvt_synth.bf16_bits(V), kvt_synth.bf16_bits(q)
+    for out in (a, b):
+        for bb, S in enumerate(lens):
+            for h in range(2):
+                ref = oracle.decode_reference(1, 4, 2, 32, 32, D, Kb[bb, h, :S], Vb[bb, h, :S], qb[bb, 4 * h:4 * h + 4],
+                                              1 / math.sqrt(D))
+                assert rel_row_err(out[bb, 4 * h:4 * h + 4].cpu().numpy(), ref).max() <= TOL
+    assert (a - b).abs().max().item() <= 5e-4 * a.abs().max().item()
 
 
 @pytest.mark.parametrize("n_shards", [2, 4])
@@ -190,8 +198,9 @@ def test_sensitivity_parity(kvt, oracle, mode, R):
     V = kvt_synth.values((H_kv, S, D), seed=52)
     Q = kvt_synth.queries((H_kv * g, T_q, D), seed=53)
     pairs = [(kb, vb) for kb in (2, 4, 8) for vb in (2, 4, 8)] + [(16, 16)]
-    got = kvt.layer_sensitivity(mode, 32, R, Q.cuda(), K.cuda(), V.cuda(), S - T_q, pairs).cpu().numpy()
+    scale = float(np.float32(1 / math.sqrt(D)))          # the ABI takes an fp32 softmax scale
+    got = kvt.layer_sensitivity(mode, 32, R, Q.cuda(), K.cuda(), V.cuda(), S - T_q, pairs, scale=scale).cpu().numpy()
     ref = oracle.sensitivity(mode, 32, R, kvt_synth.bf16_bits(Q), kvt_synth.bf16_bits(K), kvt_synth.bf16_bits(V),
-                             S - T_q, pairs, 1 / math.sqrt(D))
+                             S - T_q, pairs, scale)
     np.testing.assert_allclose(got, ref, rtol=1e-9, atol=1e-15)
     assert np.all(got[-1] == 0)
