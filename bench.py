@@ -34,6 +34,8 @@ WORKLOADS = {
     "qwen-3.92": ("configs/qwen2.5-7b_kivi_3.92.json", (28, 4, 28), 64, 8192),
     "llama-kv8": (None, (32, 8, 32), 64, 8192),
     "qwen-kv8": (None, (28, 4, 28), 64, 8192),
+    # config 5: 128k context, sequence-sharded over the ranks (partial -> NCCL all-gather -> combine)
+    "llama-128k-seqshard": ("configs/llama-3.1-8b_kivi_3.25.json", (32, 8, 32), 8, 131072),
 }
 D = 128
 
@@ -55,6 +57,7 @@ def parse():
 
 def layer_specs(name, kvt):
     cfg_path, (L, H, Hq), B, S = WORKLOADS[name]
+    name = name.replace("-128k-seqshard", "-3.25")
     if cfg_path is None:
         return [kvt.LayerSpec.kivi(8, 8) for _ in range(L)], "uniform KIVI-KV8 (baseline of P:538)"
     cfg = kvt.load_config(str(ROOT / cfg_path))
@@ -152,11 +155,14 @@ def measured_peaks():
 
 
 def ncu_traffic(workload):
+    """dram read+write bytes per launch of the profiled decode kernel (one ncu --set full capture,
+    profiles/ncu_traffic.json) — compare with that launch's algorithmic bytes, not the step average."""
     p = ROOT / "profiles" / "ncu_traffic.json"
     if p.exists():
-        j = json.loads(p.read_text())
-        return j.get(workload)
-    return None
+        j = json.loads(p.read_text()).get(workload)
+        if j:
+            return j["traffic_bytes_per_launch"], j
+    return None, None
 
 
 # ------------------------------------------------------------------------------------------------
@@ -238,9 +244,18 @@ def run_kvt(args):
     _, (L, H, Hq), B, S_ctx = WORKLOADS[args.workload]
     B = args.batch or B
     S_ctx = args.ctx or S_ctx
+    seqshard = args.workload.endswith("seqshard")
     S0 = S_ctx - 1                                           # prefilled; the first timed append makes S_ctx
     n_steps_total = args.warmup + args.steps + (0 if args.no_e2e else args.warmup + args.steps)
-    cap = ((S0 + n_steps_total + 1 + 63) // 64) * 64
+    appends = True
+    if seqshard:                                             # a6: this rank holds tokens [lo, hi) of every sequence
+        from paper_2502_04420_b200.seqshard import shard_bounds, shard_spec
+
+        lo, hi = shard_bounds(S0, world, rank)
+        S0 = hi - lo
+        appends = rank == world - 1                          # the newest tokens (and the residual) live on the last rank
+        specs = [shard_spec(sp, rank, world) for sp in specs]
+    cap = ((S0 + (n_steps_total if appends else 0) + 1 + 63) // 64) * 64
 
     # ---- build the caches: prefill S0 tokens per sequence through the append kernel ----
     gen = torch.Generator(device=dev)
@@ -268,21 +283,37 @@ def run_kvt(args):
     ws = torch.zeros(max(ws_bytes, 16), dtype=torch.uint8, device=dev)      # split counters start at zero
     n_combine = 0     # the tensor-core kernel merges its splits in-kernel (last CTA); see launches.csv
     len_before = torch.full((B,), S0, dtype=torch.int32, device=dev)
-    len_after = torch.full((B,), S0 + 1, dtype=torch.int32, device=dev)
+    len_after = torch.full((B,), S0 + (1 if appends else 0), dtype=torch.int32, device=dev)
     ones = torch.ones(B, dtype=torch.int32, device=dev)
     scale = 1.0 / math.sqrt(D)
     stream = torch.cuda.current_stream()
+    if seqshard:
+        part = torch.empty(B, Hq, D + 2, dtype=torch.float32, device=dev)
+        gathered = torch.empty(world, B, Hq, D + 2, dtype=torch.float32, device=dev)
 
     def step(ev=None):
         for l in range(L):
-            kvt.quantize_append(caches[l], k_new[l], v_new[l], len_before, ones, n_new_max=1, stream=stream)
+            if appends:
+                kvt.quantize_append(caches[l], k_new[l], v_new[l], len_before, ones, n_new_max=1, stream=stream)
             if ev is not None:
                 ev[l][0].record(stream)
-            kvt.decode_attention(caches[l], q[l], len_after, scale=scale, out=outs[l], workspace=ws, stream=stream)
-            if ev is not None:
-                ev[l][1].record(stream)
-        len_before.add_(1)
-        len_after.add_(1)
+            if seqshard:
+                kvt.decode_attention_partial(caches[l], q[l], len_after, scale=scale, partial=part, workspace=ws,
+                                             stream=stream)
+                if ev is not None:
+                    ev[l][1].record(stream)
+                if world > 1:
+                    dist.all_gather_into_tensor(gathered, part)
+                else:
+                    gathered[0].copy_(part)
+                kvt.combine_partials(gathered, out=outs[l], stream=stream)
+            else:
+                kvt.decode_attention(caches[l], q[l], len_after, scale=scale, out=outs[l], workspace=ws, stream=stream)
+                if ev is not None:
+                    ev[l][1].record(stream)
+        if appends:
+            len_before.add_(1)
+            len_after.add_(1)
 
     for _ in range(args.warmup):
         step()
@@ -295,7 +326,7 @@ def run_kvt(args):
     evs = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)] for _ in range(L)]
            for _ in range(args.steps)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    S_first = S0 + args.warmup + 1
+    S_first = S0 + (args.warmup + 1 if appends else 0)
     sampler = ClockSampler(dev.index) if not args.profile else None
     if sampler:
         sampler.__enter__()
@@ -318,12 +349,13 @@ def run_kvt(args):
     # roofline of the dominant kernel (decode attention, all layers): algorithmic bytes / event time
     alg = 0
     for i in range(args.steps):
-        S = S_first + i
+        S = S_first + (i if appends else 0)
         alg += sum(algorithmic_bytes(s, B, H, Hq, S) for s in specs)
     achieved = alg / (attn_ms / 1000.0) / 1e9
     peak, peak_src = measured_peaks()
+    traffic, traffic_src = ncu_traffic(args.workload)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": ncu_traffic(args.workload), "kernel": "decode_kernel (+combine)",
+                "traffic": traffic, "traffic_source": traffic_src, "kernel": "decode attention (all layers)",
                 "attn_share_of_step": attn_ms / ms, "peak_source": peak_src,
                 "algorithmic_bytes_per_step": alg / args.steps}
 
@@ -375,14 +407,17 @@ def run_kvt(args):
     if rank == 0:
         line = {"metric": "decode tokens/s (attention-only, mixed-precision KV)", "value": value, "unit": "tokens/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32 (bf16 in/out)",
+                "higher_is_better": True, "scaling": "strong" if seqshard else "weak", "vs_baseline": None,
+                "dtype": "fp32 (bf16 in/out)",
                 "data": "synthetic (N(0,1) K with x11 outliers on channels c%8==0, N(0,1) V, 0.5 N(0,1) q)",
                 "config": {"workload": args.workload, "layers": desc, "shape": {"L": L, "H_kv": H, "H_q": Hq, "d": D},
                            "batch_per_gpu": B, "ctx": f"{S_first}..{S_first + args.steps - 1}",
-                           "parallelism": f"batch-partitioned x{world} (no collective)",
+                           "parallelism": (f"sequence-sharded x{world} (partial -> NCCL all-gather -> combine)" if seqshard
+                                           else f"batch-partitioned x{world} (no collective)"),
                            "l2": "inputs larger than L2 (cache %.1f GB/GPU)" % (sum(c.nbytes for c in caches) / 1e9)},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": args.steps * (2 * L + n_combine), "clocks": clocks,
+                "gpu_launches": args.steps * ((1 if appends else 0) * L + L + (L if seqshard else 0) + n_combine),
+                "clocks": clocks,
                 "gb_per_s_attention": achieved}
         print(json.dumps(line))
     if world > 1:

@@ -1,0 +1,61 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py times (B = 64 sequences,
+8 KV heads, 8k context, prefill through K1, then decode appends of one token; decode planned from the
+capacity without host lengths): sampled (b, h) slices are checked against the oracle — packed bytes
+bit-exact and the fp32 output within 2e-3 normalised (A17)."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import kvt_synth
+from tests.gpu_helpers import TOL, compare_slice, rel_row_err
+
+pytestmark = pytest.mark.gpu
+D = 128
+
+
+@pytest.fixture(scope="module")
+def kvt():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2502_04420_b200 as k
+
+    return k
+
+
+@pytest.mark.parametrize("kb,vb,H,g,B", [(4, 2, 8, 4, 64), (8, 4, 8, 4, 64), (2, 2, 8, 4, 64), (8, 8, 4, 7, 32),
+                                         (4, 4, 4, 7, 32)])
+def test_fullsize_sampled(kvt, oracle, kb, vb, H, g, B):
+    S0, n_dec = 8191, 3                      # prefill 8191 tokens, then 3 decode steps (crosses a K flush)
+    spec = kvt.LayerSpec.kivi(kb, vb)
+    cap = 8192 + 64
+    dev = torch.device("cuda")
+    gen = torch.Generator(device=dev).manual_seed(1234 + kb * 10 + vb)
+    K = torch.randn(B, H, S0 + n_dec, D, device=dev, generator=gen)
+    K[..., ::8] *= 11.0
+    K = K.to(torch.bfloat16)
+    V = torch.randn(B, H, S0 + n_dec, D, device=dev, generator=gen).to(torch.bfloat16)
+    q = (0.5 * torch.randn(B, H * g, D, device=dev, generator=gen)).to(torch.bfloat16)
+    cache = kvt.LayerCache(spec, B, H, D, cap)
+    kvt.quantize_append(cache, K[:, :, :S0], V[:, :, :S0], torch.zeros(B, dtype=torch.int32, device=dev),
+                        torch.full((B,), S0, dtype=torch.int32, device=dev), n_new_max=S0)
+    lb = torch.full((B,), S0, dtype=torch.int32, device=dev)
+    ones = torch.ones(B, dtype=torch.int32, device=dev)
+    ws = torch.zeros(max(kvt.decode_workspace_bytes(cache, H * g, None), 16), dtype=torch.uint8, device=dev)
+    for i in range(n_dec):
+        kvt.quantize_append(cache, K[:, :, S0 + i:S0 + i + 1], V[:, :, S0 + i:S0 + i + 1], lb, ones, n_new_max=1)
+        lb += 1
+        out = kvt.decode_attention(cache, q, lb, scale=1 / math.sqrt(D), out_dtype=torch.float32, workspace=ws)
+    torch.cuda.synchronize()
+    S = S0 + n_dec
+    rng = np.random.default_rng(kb * 100 + vb)
+    samples = [(0, 0), (B - 1, H - 1)] + [(int(rng.integers(B)), int(rng.integers(H))) for _ in range(2)]
+    for b, h in samples:
+        Kb = kvt_synth.bf16_bits(K[b, h, :S])
+        Vb = kvt_synth.bf16_bits(V[b, h, :S])
+        compare_slice(oracle, cache, spec, b, h, Kb, Vb, S)
+        ref = oracle.decode_reference(spec.mode, kb, vb, 32, 32, D, Kb, Vb,
+                                      kvt_synth.bf16_bits(q[b, h * g:(h + 1) * g]), 1 / math.sqrt(D))
+        err = rel_row_err(out[b, h * g:(h + 1) * g].cpu().numpy(), ref)
+        assert err.max() <= TOL, f"(b={b}, h={h}): normalised error {err.max():.2e}"
