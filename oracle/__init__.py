@@ -162,18 +162,30 @@ BUFFER_NAMES = ("k_codes", "k_meta", "k_resid", "v_codes", "v_meta", "v_resid")
 _BUF_DTYPES = (np.uint8, np.uint32, np.uint16, np.uint8, np.uint32, np.uint16)
 
 
-def build_cache(mode, kb, vb, G, R, d, cap, K_bf16, V_bf16):
-    """O2 for one (b, h) slice: K, V uint16 [S][d] → dict of the six buffers (numpy)."""
+def build_cache(mode, kb, vb, G, R, d, cap, K_bf16, V_bf16, fill=0):
+    """O2 for one (b, h) slice: K, V uint16 [S][d] → dict of the six buffers (numpy).  Bytes the
+    layout does not define for this history keep the value `fill` (build twice with different fills
+    to get the mask of defined bytes)."""
     K = _u16(K_bf16).reshape(-1, d)
     V = _u16(V_bf16).reshape(-1, d)
     S = K.shape[0]
     assert V.shape[0] == S
     sz = slice_bytes(mode, kb, vb, G, R, d, cap)
-    bufs = [np.zeros(max(n // np.dtype(t).itemsize, 1), t) for n, t in zip(sz, _BUF_DTYPES)]
+    bufs = [np.full(max(n // np.dtype(t).itemsize, 1), 0, t) for n, t in zip(sz, _BUF_DTYPES)]
+    for b in bufs:
+        b.view(np.uint8)[:] = fill
     rc = lib().kvto_build_cache(mode, kb, vb, G, R, d, cap, S, _p(K), _p(V), *[_p(b) for b in bufs])
     if rc != 0:
         raise ValueError("kvto_build_cache rejected its arguments")
     return dict(zip(BUFFER_NAMES, bufs))
+
+
+def defined_bytes(mode, kb, vb, G, R, d, cap, K_bf16, V_bf16):
+    """(bytes, mask) per buffer: the oracle's bytes and which of them the layout defines for this
+    history (those identical under two different fill values)."""
+    a = build_cache(mode, kb, vb, G, R, d, cap, K_bf16, V_bf16, fill=0x00)
+    b = build_cache(mode, kb, vb, G, R, d, cap, K_bf16, V_bf16, fill=0xFF)
+    return {n: (a[n].view(np.uint8), a[n].view(np.uint8) == b[n].view(np.uint8)) for n in BUFFER_NAMES}
 
 
 def dequant_cache(mode, kb, vb, G, R, d, cap, S, bufs):

@@ -156,11 +156,57 @@ int kvto_slice_bytes(int mode, int kb, int vb, int G, int R, int d, int cap, siz
     return 0;
 }
 
+/* Blocked value layout: in KIVI mode with G = 32, d = 128 and 2/4/8-bit keys and values, each
+ * 32-token block of value codes keeps the bytes of its 32 token-major rows but reorders them so that a
+ * token t (tau = t mod 32, ks = tau / 16, r = tau mod 16) and the token 8 positions later share
+ * 32-bit words.  A "chunk" (gam, i) is the 4 channels 32 gam + 4 i .. + 3 of one token (4·bits bits,
+ * the same bits as in the packed row).  This function returns the byte offset inside the block of
+ * byte k of chunk (gam, i) of token tau. */
+static size_t vblk_byte(int bits, int tau, int gam, int i, int k) {
+    int ks = tau / 16, r = tau % 16;
+    if (bits == 2) {            /* one byte; word = [tok j, tok j+4, tok j+8, tok j+12], j = r mod 4 */
+        size_t w = ((size_t)((ks * 4 + r % 4) * 8 + i) * 4 + gam);
+        return 4 * w + 2 * (size_t)(r / 8) + (size_t)((r % 8) / 4);
+    }
+    if (bits == 4) {            /* two bytes; word = [tok j (16 bits) | tok j+8 (16 bits)], j = r mod 8 */
+        size_t w = ((size_t)((ks * 8 + r % 8) * 8 + i) * 4 + gam);
+        return 4 * w + 2 * (size_t)(r / 8) + (size_t)k;
+    }
+    /* bits == 8: four bytes (channels e = k); words [tok.c0, tok+8.c0, tok.c1, tok+8.c1], [.c2, .., .c3] */
+    size_t w = ((size_t)((ks * 8 + r % 8) * 8 + i) * 4 + gam) * 2 + (size_t)(k / 2);
+    return 4 * w + 2 * (size_t)(k % 2) + (size_t)(r / 8);
+}
+
+/* The blocked layout is used for KIVI layers whose key and value are both quantised, with G = 32 and
+ * d = 128; every other cache keeps token-major value rows. */
+static int blocked_v(int mode, int kb, int vb, int G, int d) {
+    return mode == KVTO_MODE_KIVI && kb != 16 && vb != 16 && G == 32 && d == 128;
+}
+
+/* Write the packed row of token t into the blocked value layout. */
+static void vblk_store(int bits, int t, const uint8_t* row, uint8_t* codes) {
+    uint8_t* blk = codes + (size_t)(t / 32) * 32 * (size_t)(128 * bits / 8);
+    int cb = bits / 2;          /* bytes per chunk */
+    for (int gam = 0; gam < 4; ++gam)
+        for (int i = 0; i < 8; ++i)
+            for (int k = 0; k < cb; ++k)
+                blk[vblk_byte(bits, t % 32, gam, i, k)] = row[(size_t)(32 * gam + 4 * i) * bits / 8 + k];
+}
+
+static void vblk_load(int bits, int t, const uint8_t* codes, uint8_t* row) {
+    const uint8_t* blk = codes + (size_t)(t / 32) * 32 * (size_t)(128 * bits / 8);
+    int cb = bits / 2;
+    for (int gam = 0; gam < 4; ++gam)
+        for (int i = 0; i < 8; ++i)
+            for (int k = 0; k < cb; ++k)
+                row[(size_t)(32 * gam + 4 * i) * bits / 8 + k] = blk[vblk_byte(bits, t % 32, gam, i, k)];
+}
+
 /* Per-token tensor (V in both modes, K in per-token mode): token t < n_q is split into d/G channel
- * groups, each quantised by O1 and packed into row t; tokens [n_q, S) stay bf16 in the ring slot
- * t mod R. */
+ * groups, each quantised by O1 and packed into row t (or into the blocked layout); tokens [n_q, S) stay
+ * bf16 in the ring slot t mod R. */
 static void build_per_token(int bits, int G, int R, int d, int S, const uint16_t* X,
-                            uint8_t* codes, uint32_t* meta, uint16_t* resid) {
+                            uint8_t* codes, uint32_t* meta, uint16_t* resid, int blocked) {
     int rb = row_bytes(d, bits);
     if (bits == 16) {
         for (int t = 0; t < S; ++t) memcpy(codes + (size_t)t * rb, X + (size_t)t * d, (size_t)rb);
@@ -172,7 +218,13 @@ static void build_per_token(int bits, int G, int R, int d, int S, const uint16_t
         for (int j = 0; j < d / G; ++j)
             kvto_quantize_group(X + (size_t)t * d + (size_t)j * G, G, 1, bits, tmp + j * G,
                                 meta + (size_t)t * (d / G) + j);
-        kvto_pack_row(tmp, d, bits, codes + (size_t)t * rb);
+        if (blocked) {
+            uint8_t row[128];
+            kvto_pack_row(tmp, d, bits, row);
+            vblk_store(bits, t, row, codes);
+        } else {
+            kvto_pack_row(tmp, d, bits, codes + (size_t)t * rb);
+        }
     }
     for (int t = nq; t < S; ++t)
         memcpy(resid + (size_t)(t % R) * d, X + (size_t)t * d, (size_t)d * 2);
@@ -209,13 +261,13 @@ int kvto_build_cache(int mode, int kb, int vb, int G, int R, int d, int cap, int
     if (mode == KVTO_MODE_KIVI && kb != 16)
         build_per_channel(kb, G, R, d, S, K, k_codes, k_meta, k_resid);
     else
-        build_per_token(kb, G, R, d, S, K, k_codes, k_meta, k_resid);
-    build_per_token(vb, G, R, d, S, V, v_codes, v_meta, v_resid);
+        build_per_token(kb, G, R, d, S, K, k_codes, k_meta, k_resid, 0);
+    build_per_token(vb, G, R, d, S, V, v_codes, v_meta, v_resid, blocked_v(mode, kb, vb, G, d));
     return 0;
 }
 
 static void dequant_per_token(int bits, int G, int R, int d, int S, const uint8_t* codes,
-                              const uint32_t* meta, const uint16_t* resid, double* Xh) {
+                              const uint32_t* meta, const uint16_t* resid, double* Xh, int blocked) {
     int rb = row_bytes(d, bits);
     uint8_t* tmp = (uint8_t*)malloc((size_t)d);
     if (bits == 16) {
@@ -231,7 +283,13 @@ static void dequant_per_token(int bits, int G, int R, int d, int S, const uint8_
     }
     int nq = S > R ? S - R : 0;
     for (int t = 0; t < nq; ++t) {
-        kvto_unpack_row(codes + (size_t)t * rb, d, bits, tmp);
+        if (blocked) {
+            uint8_t row[128];
+            vblk_load(bits, t, codes, row);
+            kvto_unpack_row(row, d, bits, tmp);
+        } else {
+            kvto_unpack_row(codes + (size_t)t * rb, d, bits, tmp);
+        }
         for (int c = 0; c < d; ++c)
             Xh[(size_t)t * d + c] = kvto_dequant_value(tmp[c], meta[(size_t)t * (d / G) + c / G]);
     }
@@ -264,8 +322,8 @@ int kvto_dequant_cache(int mode, int kb, int vb, int G, int R, int d, int cap, i
     if (mode == KVTO_MODE_KIVI && kb != 16)
         dequant_per_channel(kb, G, R, d, S, k_codes, k_meta, k_resid, Khat);
     else
-        dequant_per_token(kb, G, R, d, S, k_codes, k_meta, k_resid, Khat);
-    dequant_per_token(vb, G, R, d, S, v_codes, v_meta, v_resid, Vhat);
+        dequant_per_token(kb, G, R, d, S, k_codes, k_meta, k_resid, Khat, 0);
+    dequant_per_token(vb, G, R, d, S, v_codes, v_meta, v_resid, Vhat, blocked_v(mode, kb, vb, G, d));
     return 0;
 }
 

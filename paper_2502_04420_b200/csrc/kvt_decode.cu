@@ -74,12 +74,6 @@ struct Instance {
     int occ = 1;
 };
 
-// KVT_DECODE_GENERIC=1 forces the CUDA-core kernel everywhere (A/B testing of the two kernels).
-static bool dec_force_generic() {
-    static const bool v = [] { const char* e = getenv("KVT_DECODE_GENERIC"); return e && e[0] == '1'; }();
-    return v;
-}
-
 static int bits_index(int b) { return b == 2 ? 0 : b == 4 ? 1 : b == 8 ? 2 : 3; }
 
 // Per-device cache of (function, smem, occupancy) for each instance; configured once.
@@ -131,6 +125,8 @@ static int32_t get_instance(int kb, int vb, int kind, int GM, Instance* out, int
 
 // Number of KV splits: enough CTAs for ~4 waves of resident CTAs, at least 16 tiles per split.
 static int plan_splits(const Geometry& g, int plan_len, int occ, int sms) {
+    static const int forced = [] { const char* e = getenv("KVT_NSPLIT"); return e ? atoi(e) : 0; }();
+    if (forced > 0) return forced;                      // experiments only
     int n_tiles = (plan_len + kTile - 1) / kTile;
     long long base = (long long)g.B * g.H;
     long long target = 4LL * sms * occ;
@@ -142,10 +138,10 @@ static int plan_splits(const Geometry& g, int plan_len, int occ, int sms) {
     return n;
 }
 
-// The tensor-core kernel covers KIVI layers with G = 32 and 2/4/8-bit K and V; everything else runs
-// the generic CUDA-core kernel.
+// The tensor-core kernel covers exactly the caches with the blocked value layout (KIVI, G = 32, 2/4/8-bit
+// K and V); everything else runs the generic CUDA-core kernel.
 static int kernel_kind(const Geometry& g) {
-    if (g.key_per_channel && g.G == 32 && g.kb != 16 && g.vb != 16 && !dec_force_generic()) return 2;
+    if (g.v_blocked) return 2;
     return g.key_per_channel ? 1 : 0;
 }
 

@@ -211,11 +211,36 @@ __device__ __forceinline__ void tail_k(const Slice& s, const Geometry& g, int t,
     }
 }
 
-template <int VB>
+// The 4 codes of chunk (lane / 8, lane % 8) of token t in the blocked value layout.
+template <int BITS>
+__device__ __forceinline__ void codes4_blk(const uint8_t* vc, int t, int lane, uint32_t c[4]) {
+    const uint8_t* blk = vc + (size_t)(t >> 5) * 32 * (size_t)(16 * BITS);
+    const int tau = t & 31, gam = lane >> 3, i = lane & 7;
+    if constexpr (BITS == 2) {
+        const uint32_t w = blk[vblk_off(2, tau, gam, i, 0)];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) c[e] = (w >> (2 * e)) & 3u;
+    } else if constexpr (BITS == 4) {
+        const uint32_t w = *reinterpret_cast<const uint16_t*>(blk + vblk_off(4, tau, gam, i, 0));
+#pragma unroll
+        for (int e = 0; e < 4; ++e) c[e] = (w >> (4 * e)) & 15u;
+    } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) c[e] = blk[vblk_off(8, tau, gam, i, e)];
+    }
+}
+
+template <int VB, bool BLK = false>
 __device__ __forceinline__ void tail_v(const Slice& s, const Geometry& g, int t, int nqV, int lane, float x[4]) {
     if (t < nqV) {
         const uint8_t* row = s.vc + (size_t)t * g.row_v;
-        if constexpr (VB == 16) {
+        if constexpr (BLK && VB != 16) {
+            uint32_t c[4];
+            codes4_blk<VB>(s.vc, t, lane, c);
+            const uint32_t m = s.vm[(size_t)t * (D / g.G) + (4 * lane) / g.G];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) x[i] = fmaf((float)c[i], bf2f(m & 0xffffu), bf2f(m >> 16));
+        } else if constexpr (VB == 16) {
             bf16x4(reinterpret_cast<const uint16_t*>(row) + 4 * lane, x);
         } else {
             uint32_t c[4];

@@ -71,6 +71,9 @@ __device__ __forceinline__ Mul make_mul() {
 #ifndef KVT_MINB
 #define KVT_MINB 4
 #endif
+#ifndef KVT_EXP
+#define KVT_EXP 0      // profiling experiments only: 1 = skip PV, 2 = skip QK
+#endif
 __device__ __forceinline__ uint32_t shr8(uint32_t x, const Mul& k) {
 #if KVT_FMA_SHIFT
     uint32_t r;
@@ -137,38 +140,56 @@ __device__ __forceinline__ int k_slot_of(int cc) {
     }
 }
 
-// ---- PV A operand: channels 32γ + 4gid + e (e < 4) of tokens (T, T+8) -> 4 subnormal pairs ----------
-// h[e] = (code(T, e), code(T+8, e)) · 2^(VP(e) - 24)
+// ---- PV A operand from the blocked value layout ----------------------------------------
+// For k-step ks and the thread's two token pairs (T, T+8), T = 16ks + tig and T = 16ks + tig + 4, the
+// codes of channels 32γ + 4gid + e (e < 4) of all 4 groups are one or two LDS.128:
+//   hA[γ][e] = (code(T, e), code(T+8, e)), hB[γ][e] = the same for T + 4 — fp16 subnormals · 2^(VP(e)-24).
 template <int VB>
 __host__ __device__ constexpr int VP(int e) { return VB == 4 ? 4 * (e & 1) : (VB == 2 ? 2 * e : 0); }
 
 template <int VB>
-__device__ __forceinline__ void v_pairs(const uint8_t* r0, const uint8_t* r1, int gamma, int gid, uint32_t h[4],
-                                        const Mul& km) {
+struct VRaw {                                  // the raw blocked words of one k-step
+    uint32_t a[VB == 8 ? 8 : 4], b[VB == 2 ? 1 : (VB == 8 ? 8 : 4)];
+};
+
+template <int VB>
+__device__ __forceinline__ void v_load(const uint8_t* vblk, int ks, int tig, int gid, VRaw<VB>& r) {
+    const uint4* w4 = reinterpret_cast<const uint4*>(vblk);
     if constexpr (VB == 4) {
-        const uint32_t x0 = *reinterpret_cast<const uint16_t*>(r0 + 16 * gamma + 2 * gid);
-        const uint32_t x1 = *reinterpret_cast<const uint16_t*>(r1 + 16 * gamma + 2 * gid);
-        const uint32_t y = pack16(x0, x1, km), y8 = shr8(y, km);
-        h[0] = y & 0x000F000Fu;
-        h[1] = y & 0x00F000F0u;
-        h[2] = y8 & 0x000F000Fu;
-        h[3] = y8 & 0x00F000F0u;
+        // word ((ks*8 + j)*8 + gid)*4 + γ = [tok 16ks+j (16 bits) | tok 16ks+j+8 (16 bits)], j = tig, tig+4
+        const uint4 a = w4[(ks * 8 + tig) * 8 + gid], b = w4[(ks * 8 + tig + 4) * 8 + gid];
+        r.a[0] = a.x; r.a[1] = a.y; r.a[2] = a.z; r.a[3] = a.w;
+        r.b[0] = b.x; r.b[1] = b.y; r.b[2] = b.z; r.b[3] = b.w;
     } else if constexpr (VB == 2) {
-        const uint32_t x0 = r0[8 * gamma + gid];
-        const uint32_t x1 = r1[8 * gamma + gid];
-        const uint32_t y = pack16(x0, x1, km);             // [x0.b0, 0, x1.b0, 0]
-        h[0] = y & 0x00030003u;
-        h[1] = y & 0x000C000Cu;
-        h[2] = y & 0x00300030u;
-        h[3] = y & 0x00C000C0u;
+        // word ((ks*4 + j)*8 + gid)*4 + γ = bytes [tok j, tok j+4, tok j+8, tok j+12] (+16ks), j = tig
+        const uint4 a = w4[(ks * 4 + tig) * 8 + gid];
+        r.a[0] = a.x; r.a[1] = a.y; r.a[2] = a.z; r.a[3] = a.w;
     } else {
-        const uint32_t x0 = *reinterpret_cast<const uint32_t*>(r0 + 32 * gamma + 4 * gid);
-        const uint32_t x1 = *reinterpret_cast<const uint32_t*>(r1 + 32 * gamma + 4 * gid);
-        const uint32_t p01 = __byte_perm(x0, x1, 0x5140), p23 = __byte_perm(x0, x1, 0x7362);
-        h[0] = __byte_perm(p01, 0u, 0x4140);
-        h[1] = __byte_perm(p01, 0u, 0x4342);
-        h[2] = __byte_perm(p23, 0u, 0x4140);
-        h[3] = __byte_perm(p23, 0u, 0x4342);
+        // words (((ks*8 + j)*8 + gid)*4 + γ)*2 + {0,1} = [T.c0, T8.c0, T.c1, T8.c1], [T.c2, T8.c2, T.c3, T8.c3]
+        const uint4* pa = w4 + ((ks * 8 + tig) * 8 + gid) * 2;
+        const uint4* pb = w4 + ((ks * 8 + tig + 4) * 8 + gid) * 2;
+        const uint4 a0 = pa[0], a1 = pa[1], b0 = pb[0], b1 = pb[1];
+        r.a[0] = a0.x; r.a[1] = a0.y; r.a[2] = a0.z; r.a[3] = a0.w; r.a[4] = a1.x; r.a[5] = a1.y; r.a[6] = a1.z; r.a[7] = a1.w;
+        r.b[0] = b0.x; r.b[1] = b0.y; r.b[2] = b0.z; r.b[3] = b0.w; r.b[4] = b1.x; r.b[5] = b1.y; r.b[6] = b1.z; r.b[7] = b1.w;
+    }
+}
+
+// hA[e] = (code(T, e), code(T+8, e)), hB[e] = the same for T + 4, of group g4 — fp16 subnormals
+template <int VB>
+__device__ __forceinline__ void v_frag(const VRaw<VB>& r, int g4, uint32_t hA[4], uint32_t hB[4]) {
+    if constexpr (VB == 4) {
+        const uint32_t xa = r.a[g4], xb = r.b[g4], xa8 = xa >> 8, xb8 = xb >> 8;
+        hA[0] = xa & 0x000F000Fu; hA[1] = xa & 0x00F000F0u; hA[2] = xa8 & 0x000F000Fu; hA[3] = xa8 & 0x00F000F0u;
+        hB[0] = xb & 0x000F000Fu; hB[1] = xb & 0x00F000F0u; hB[2] = xb8 & 0x000F000Fu; hB[3] = xb8 & 0x00F000F0u;
+    } else if constexpr (VB == 2) {
+        const uint32_t x = r.a[g4], x8 = x >> 8;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) { hA[e] = x & (0x00030003u << (2 * e)); hB[e] = x8 & (0x00030003u << (2 * e)); }
+    } else {
+        hA[0] = __byte_perm(r.a[2 * g4], 0u, 0x4140); hA[1] = __byte_perm(r.a[2 * g4], 0u, 0x4342);
+        hA[2] = __byte_perm(r.a[2 * g4 + 1], 0u, 0x4140); hA[3] = __byte_perm(r.a[2 * g4 + 1], 0u, 0x4342);
+        hB[0] = __byte_perm(r.b[2 * g4], 0u, 0x4140); hB[1] = __byte_perm(r.b[2 * g4], 0u, 0x4342);
+        hB[2] = __byte_perm(r.b[2 * g4 + 1], 0u, 0x4140); hB[3] = __byte_perm(r.b[2 * g4 + 1], 0u, 0x4342);
     }
 }
 
@@ -190,23 +211,47 @@ template <int KB, int VB>
 struct Geo {
     static constexpr int KROW = 16 * KB;                 // bytes per key code row
     static constexpr int VROW = 16 * VB;
-    static constexpr int VSTR = VROW + (VB == 8 ? 32 : 16);   // padded value row (conflict-free PV loads)
-    static constexpr int K_OFF = 0;
+    static constexpr int K_OFF = 0;                      // stage = [K codes | K block meta | V block | V meta]
     static constexpr int KM_OFF = K_OFF + kTile * KROW;
     static constexpr int V_OFF = KM_OFF + D * 4;
-    static constexpr int VM_OFF = V_OFF + kTile * VSTR;
+    static constexpr int VM_OFF = V_OFF + kTile * VROW;
     static constexpr int STAGE = VM_OFF + kTile * 16;
-    static constexpr int NS = 2;                         // double buffer: a tile takes ~3k cycles, far above DRAM latency
+#ifndef KVT_NS
+#define KVT_NS 2
+#endif
+    static constexpr int NS = KVT_NS;                    // cp.async ring depth per warp
     // per warp: ring + PV weight tile (half2 [4 γ][2 ks][8 pairs][8 heads]) + key scale slots (half2 [4][16])
     static constexpr int W_OFF = NS * STAGE;
     static constexpr int W_BYTES = 4 * 2 * 8 * 8 * 4;
     static constexpr int SH_OFF = W_OFF + W_BYTES;
-    static constexpr int WARP_BYTES = SH_OFF + 4 * 16 * 4;
+    static constexpr int BAR_OFF = SH_OFF + 4 * 16 * 4;           // one mbarrier per stage
+    static constexpr int WARP_BYTES = BAR_OFF + 8 * NS;
     static constexpr int Q_BYTES = 8 * D * 4;            // q fp32 [8][128]
     static constexpr int COMB_BYTES = 2 * kWarps * 8 * (2 + D) * 4;
     static constexpr int BODY = kWarps * WARP_BYTES > COMB_BYTES ? kWarps * WARP_BYTES : COMB_BYTES;
     static constexpr size_t SMEM = (size_t)Q_BYTES + BODY;
 };
+
+// ---- TMA bulk copies (cp.async.bulk) completing on a per-stage mbarrier ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)), "r"(phase));
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
 __device__ __forceinline__ void cp16(void* s, const void* g) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(s);
@@ -218,7 +263,7 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 
 // GM: 4 (g <= 4: n = 4 heads x {hi, lo}) or 8 (g <= 8: separate hi and lo MMAs).
 template <int KB, int VB, int GM>
-__global__ void __launch_bounds__(kThreads, KVT_MINB) decode_mma_kernel(DecodeArgs a) {
+__global__ void __launch_bounds__(kThreads, GM == 4 ? KVT_MINB : 3) decode_mma_kernel(DecodeArgs a) {
     using Gm = Geo<KB, VB>;
     extern __shared__ __align__(16) uint8_t smem[];
     float* q_s = reinterpret_cast<float*>(smem);                           // [8][128]
@@ -306,35 +351,36 @@ __global__ void __launch_bounds__(kThreads, KVT_MINB) decode_mma_kernel(DecodeAr
     for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.0f;
     int kp = 126;                  // PV weight exponent (only decreases)
 
+    // ---- per-warp TMA ring: lane 0 issues four bulk copies per tile onto the stage's mbarrier ----
+    uint64_t* bars = reinterpret_cast<uint64_t*>(wbase + Gm::BAR_OFF);
+    if (lane == 0) {
+#pragma unroll
+        for (int st = 0; st < Gm::NS; ++st) mbar_init(bars + st);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncwarp();
     auto issue = [&](int it, int st) {
+        if (lane != 0) return;
         const int t0 = (tile_lo + warp + it * kWarps) * kTile;
         uint8_t* sb = wbase + st * Gm::STAGE;
-        const uint8_t* gk = sl.kc + (size_t)t0 * Gm::KROW;
-#pragma unroll
-        for (int c = lane; c < kTile * Gm::KROW / 16; c += 32) cp16(sb + Gm::K_OFF + 16 * c, gk + 16 * c);
-        cp16(sb + Gm::KM_OFF + 16 * lane, reinterpret_cast<const uint8_t*>(sl.km + (size_t)(t0 / kTile) * D) + 16 * lane);
-        const uint8_t* gv = sl.vc + (size_t)t0 * Gm::VROW;
-#pragma unroll
-        for (int c = lane; c < kTile * Gm::VROW / 16; c += 32) {
-            const int row = c / (Gm::VROW / 16), col = c % (Gm::VROW / 16);
-            cp16(sb + Gm::V_OFF + row * Gm::VSTR + 16 * col, gv + 16 * c);
-        }
-        cp16(sb + Gm::VM_OFF + 16 * lane, reinterpret_cast<const uint8_t*>(sl.vm + (size_t)t0 * 4) + 16 * lane);
+        fence_proxy_async();                      // the stage's previous generic-proxy reads come first
+        mbar_expect_tx(bars + st, Gm::STAGE);
+        bulk_g2s(sb + Gm::K_OFF, sl.kc + (size_t)t0 * Gm::KROW, kTile * Gm::KROW, bars + st);
+        bulk_g2s(sb + Gm::KM_OFF, sl.km + (size_t)(t0 / kTile) * D, D * 4, bars + st);
+        bulk_g2s(sb + Gm::V_OFF, sl.vc + (size_t)t0 * Gm::VROW, kTile * Gm::VROW, bars + st);
+        bulk_g2s(sb + Gm::VM_OFF, sl.vm + (size_t)t0 * 4, kTile * 16, bars + st);
     };
 
 #pragma unroll
-    for (int s = 0; s < Gm::NS - 1; ++s) {
+    for (int s = 0; s < Gm::NS - 1; ++s)
         if (s < n_my) issue(s, s);
-        cp_commit();
-    }
     for (int it = 0; it < n_my; ++it) {
         {
             const int nx = it + Gm::NS - 1;
             if (nx < n_my) issue(nx, nx % Gm::NS);
-            cp_commit();
         }
-        cp_wait<Gm::NS - 1>();
-        __syncwarp();
+        mbar_wait(bars + (it % Gm::NS), (uint32_t)((it / Gm::NS) & 1));
+        if (KVT_EXP == 4) { __syncwarp(); continue; }       // experiment: stream the tiles only
         const uint8_t* sb = wbase + (it % Gm::NS) * Gm::STAGE;
         const uint8_t* kc_s = sb + Gm::K_OFF;
         const uint32_t* km_s = reinterpret_cast<const uint32_t*>(sb + Gm::KM_OFF);
@@ -430,8 +476,8 @@ __global__ void __launch_bounds__(kThreads, KVT_MINB) decode_mma_kernel(DecodeAr
             }
         }
         // (3) QK on the tensor cores: two m-tiles of 16 tokens, 4 independent accumulator chains
-        float dq[2][4];
-        {
+        float dq[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+        if (KVT_EXP != 2 && KVT_EXP != 3) {
             uint32_t w[4][KB];        // rows gid, gid+8, 16+gid, 24+gid
 #pragma unroll
             for (int rr = 0; rr < 4; ++rr) {
@@ -562,7 +608,7 @@ __global__ void __launch_bounds__(kThreads, KVT_MINB) decode_mma_kernel(DecodeAr
         }
         __syncwarp();
         // (6) PV on the tensor cores: 8 m-tiles (γ, μ) x 2 k-steps of 16 tokens
-        {
+        if (KVT_EXP != 1 && KVT_EXP != 3) {
             if (__any_sync(kFull, resc)) {
                 const float r0 = alpha[0] * kfac, r1 = alpha[1] * kfac;   // PV columns 2tig, 2tig+1
 #pragma unroll
@@ -570,17 +616,14 @@ __global__ void __launch_bounds__(kThreads, KVT_MINB) decode_mma_kernel(DecodeAr
             }
 #pragma unroll
             for (int ks = 0; ks < 2; ++ks) {
-                const uint8_t* vr0 = vc_s + (16 * ks + tig) * Gm::VSTR;       // tokens T = 16ks + tig, T + 8
-                const uint8_t* vr1 = vr0 + 8 * Gm::VSTR;
-                const uint8_t* vr2 = vr0 + 4 * Gm::VSTR;                       // tokens T + 4, T + 12
-                const uint8_t* vr3 = vr2 + 8 * Gm::VSTR;
+                VRaw<VB> raw;
+                v_load<VB>(vc_s, ks, tig, gid, raw);
 #pragma unroll
                 for (int gam = 0; gam < 4; ++gam) {
                     const uint32_t* wr = w_s + (gam * 2 + ks) * 64 + gid;
                     const uint32_t b0 = wr[tig * 8], b1 = wr[(tig + 4) * 8];
                     uint32_t hA4[4], hB4[4];
-                    v_pairs<VB>(vr0, vr1, gam, gid, hA4, kmul);
-                    v_pairs<VB>(vr2, vr3, gam, gid, hB4, kmul);
+                    v_frag<VB>(raw, gam, hA4, hB4);
                     hmma(o[2 * gam], hA4[0], hA4[1], hB4[0], hB4[1], b0, b1);
                     hmma(o[2 * gam + 1], hA4[2], hA4[3], hB4[2], hB4[3], b0, b1);
                 }
@@ -588,8 +631,12 @@ __global__ void __launch_bounds__(kThreads, KVT_MINB) decode_mma_kernel(DecodeAr
         }
         __syncwarp();
     }
-    cp_wait<0>();
 
+    __syncwarp();
+    if (lane == 0) {
+#pragma unroll
+        for (int st = 0; st < Gm::NS; ++st) asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bars + st)));
+    }
     // ---- warp epilogue: l over the 8 row-groups, zero sums, o = D * 2^(24 - P(row) - kp) + zacc ----
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
@@ -646,24 +693,48 @@ __global__ void __launch_bounds__(kThreads, KVT_MINB) decode_mma_kernel(DecodeAr
             ot[h][0] = ot[h][1] = ot[h][2] = ot[h][3] = 0.0f;
         }
         if (split == a.n_split - 1) {
-            for (int t = n_main + warp; t < S; t += kWarps) {
-                float kx[4], vx[4];
-                dec::tail_k<KB, true>(sl, g, t, nqK, lane, kx);
-                dec::tail_v<VB>(sl, g, t, nqV, lane, vx);
+            // four tokens per iteration: all loads first, then four independent dot/shuffle chains
+            for (int t0 = n_main + warp; t0 < S; t0 += 4 * kWarps) {
+                float kx[4][4], vx[4][4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int t = t0 + u * kWarps;
+                    if (t < S) {
+                        dec::tail_k<KB, true>(sl, g, t, nqK, lane, kx[u]);
+                        dec::tail_v<VB, true>(sl, g, t, nqV, lane, vx[u]);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) kx[u][i] = vx[u][i] = 0.0f;
+                    }
+                }
+                float sc[4][GM];
 #pragma unroll
                 for (int h = 0; h < GM; ++h) {
                     const float4 qv = *reinterpret_cast<const float4*>(q_s + h * D + 4 * lane);
-                    float s = qv.x * kx[0] + qv.y * kx[1] + qv.z * kx[2] + qv.w * kx[3];
 #pragma unroll
-                    for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(kFull, s, off);
-                    s *= a.scale_log2;
-                    const float mn = fmaxf(mt_[h], s);
-                    const float al = exp2f(mt_[h] - mn);
-                    const float pp = exp2f(s - mn);
-                    lt[h] = lt[h] * al + pp;
+                    for (int u = 0; u < 4; ++u)
+                        sc[u][h] = qv.x * kx[u][0] + qv.y * kx[u][1] + qv.z * kx[u][2] + qv.w * kx[u][3];
+                }
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) ot[h][i] = ot[h][i] * al + pp * vx[i];
-                    mt_[h] = mn;
+                for (int off = 16; off >= 1; off >>= 1)
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+#pragma unroll
+                        for (int h = 0; h < GM; ++h) sc[u][h] += __shfl_xor_sync(kFull, sc[u][h], off);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (t0 + u * kWarps >= S) break;
+#pragma unroll
+                    for (int h = 0; h < GM; ++h) {
+                        const float sv = sc[u][h] * a.scale_log2;
+                        const float mn = fmaxf(mt_[h], sv);
+                        const float al = exp2f(mt_[h] - mn);
+                        const float pp = exp2f(sv - mn);
+                        lt[h] = lt[h] * al + pp;
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) ot[h][i] = ot[h][i] * al + pp * vx[u][i];
+                        mt_[h] = mn;
+                    }
                 }
             }
         }
@@ -705,9 +776,9 @@ __global__ void __launch_bounds__(kThreads, KVT_MINB) decode_mma_kernel(DecodeAr
     // ---- fused split combine (K3): the last CTA of this (b, kv head) to arrive merges the partials ----
     if (a.out_mode == 3 && a.counters != nullptr) {
         __shared__ int is_last;
-        __syncthreads();
+        __threadfence();                      // every thread's partial writes are visible device-wide ...
+        __syncthreads();                      // ... before thread 0 announces this split
         if (tid == 0) {
-            __threadfence();
             const int old = atomicAdd(a.counters + bh, 1);
             is_last = (old == a.n_split - 1);
         }

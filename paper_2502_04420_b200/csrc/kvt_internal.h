@@ -30,9 +30,27 @@ __host__ __device__ inline int nq_key(int mode, int bits, int G, int R, int S) {
 }
 __host__ __device__ inline int row_bytes(int d, int bits) { return bits == 16 ? 2 * d : d * bits / 8; }
 
+// Blocked value layout: byte offset, inside a 32-token block, of byte k of chunk
+// (gam, i) = channels 32 gam + 4 i .. + 3 of the token at position tau of the block.  Tokens tau and
+// tau + 8 of each 16-token half share 32-bit words, so the PV operand pairs load directly.
+__host__ __device__ inline uint32_t vblk_off(int bits, int tau, int gam, int i, int k) {
+    const int ks = tau >> 4, r = tau & 15;
+    if (bits == 2) {
+        const uint32_t w = (uint32_t)(((ks * 4 + (r & 3)) * 8 + i) * 4 + gam);
+        return 4 * w + 2 * (uint32_t)(r >> 3) + (uint32_t)((r & 7) >> 2);
+    }
+    if (bits == 4) {
+        const uint32_t w = (uint32_t)(((ks * 8 + (r & 7)) * 8 + i) * 4 + gam);
+        return 4 * w + 2 * (uint32_t)(r >> 3) + (uint32_t)k;
+    }
+    const uint32_t w = (uint32_t)((((ks * 8 + (r & 7)) * 8 + i) * 4 + gam) * 2 + (k >> 1));
+    return 4 * w + 2 * (uint32_t)(k & 1) + (uint32_t)(r >> 3);
+}
+
 struct Geometry {
     int mode, kb, vb, G, R, F, d, cap, B, H;
     bool key_per_channel;          // KIVI key with bits < 16
+    bool v_blocked;                // blocked value layout (KIVI, K and V quantised, G = 32, d = 128; §4)
     size_t row_k, row_v;           // bytes per token row
     size_t kc, km, kr, vc, vm, vr; // bytes per (b,h) slice
 };

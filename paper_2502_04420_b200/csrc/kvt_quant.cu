@@ -77,7 +77,8 @@ __device__ void quant_block_warp(Src src, int G, int bits, uint8_t* codes0, size
 // phase 2: ring writes (chunk 0 only, after phase 0).
 __device__ void per_token_tensor(int phase, int bits, int G, int R, int L0, int S, const uint16_t* in,
                                  int64_t s2, uint8_t* codes, size_t row_bytes, uint32_t* meta, uint16_t* ring,
-                                 int wid, int nwarps, int lane) {
+                                 int wid, int nwarps, int lane, bool blocked = false) {
+    uint8_t* vblk = blocked ? codes : nullptr;
     const int gpr = 128 / G;   // groups per row
     if (bits == 16) {
         if (phase != 1) return;
@@ -93,13 +94,13 @@ __device__ void per_token_tensor(int phase, int bits, int G, int R, int L0, int 
         int hi = q1 < L0 ? q1 : L0;
         for (int t = q0 + wid; t < hi; t += nwarps) {
             uint2 v = reinterpret_cast<const uint2*>(ring + (size_t)(t % R) * 128)[lane];
-            quant_row_warp(v, bits, G, codes + (size_t)t * row_bytes, meta + (size_t)t * gpr, lane);
+            quant_row_warp(v, bits, G, codes + (size_t)t * row_bytes, meta + (size_t)t * gpr, lane, vblk, t);
         }
     } else if (phase == 1) {
         int lo = q0 > L0 ? q0 : L0;
         for (int t = lo + wid; t < q1; t += nwarps) {
             uint2 v = reinterpret_cast<const uint2*>(in + (int64_t)(t - L0) * s2)[lane];
-            quant_row_warp(v, bits, G, codes + (size_t)t * row_bytes, meta + (size_t)t * gpr, lane);
+            quant_row_warp(v, bits, G, codes + (size_t)t * row_bytes, meta + (size_t)t * gpr, lane, vblk, t);
         }
     } else if (R > 0) {
         int lo = (S - R) > L0 ? (S - R) : L0;
@@ -164,14 +165,14 @@ __global__ void __launch_bounds__(kWarps * 32) append_kernel(AppendArgs a) {
             per_channel_key(0, g.kb, g.G, g.F, L0, S, kin, a.s2, kc, g.row_k, km, kr, warp, kWarps, lane);
         else
             per_token_tensor(0, g.kb, g.G, g.R, L0, S, kin, a.s2, kc, g.row_k, km, kr, warp, kWarps, lane);
-        per_token_tensor(0, g.vb, g.G, g.R, L0, S, vin, a.s2, vc, g.row_v, vm, vr, warp, kWarps, lane);
+        per_token_tensor(0, g.vb, g.G, g.R, L0, S, vin, a.s2, vc, g.row_v, vm, vr, warp, kWarps, lane, g.v_blocked);
     }
     const int wid = chunk * kWarps + warp, nw = gridDim.x * kWarps;
     if (g.key_per_channel)
         per_channel_key(1, g.kb, g.G, g.F, L0, S, kin, a.s2, kc, g.row_k, km, kr, wid, nw, lane);
     else
         per_token_tensor(1, g.kb, g.G, g.R, L0, S, kin, a.s2, kc, g.row_k, km, kr, wid, nw, lane);
-    per_token_tensor(1, g.vb, g.G, g.R, L0, S, vin, a.s2, vc, g.row_v, vm, vr, wid, nw, lane);
+    per_token_tensor(1, g.vb, g.G, g.R, L0, S, vin, a.s2, vc, g.row_v, vm, vr, wid, nw, lane, g.v_blocked);
     // phase 2 (chunk 0): new residual tokens, after every residual read of phase 0
     if (chunk == 0) {
         __syncthreads();
@@ -179,7 +180,7 @@ __global__ void __launch_bounds__(kWarps * 32) append_kernel(AppendArgs a) {
             per_channel_key(2, g.kb, g.G, g.F, L0, S, kin, a.s2, kc, g.row_k, km, kr, warp, kWarps, lane);
         else
             per_token_tensor(2, g.kb, g.G, g.R, L0, S, kin, a.s2, kc, g.row_k, km, kr, warp, kWarps, lane);
-        per_token_tensor(2, g.vb, g.G, g.R, L0, S, vin, a.s2, vc, g.row_v, vm, vr, warp, kWarps, lane);
+        per_token_tensor(2, g.vb, g.G, g.R, L0, S, vin, a.s2, vc, g.row_v, vm, vr, warp, kWarps, lane, g.v_blocked);
     }
 }
 

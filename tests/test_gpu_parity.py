@@ -36,6 +36,9 @@ SPECS = [
     ("pt_k4v8_g128_r32", lambda k: k.LayerSpec.per_token(4, 8, group=128, residual=32)),
     ("kivi_k4v2", lambda k: k.LayerSpec.kivi(4, 2)),
     ("kivi_k8v8", lambda k: k.LayerSpec.kivi(8, 8)),
+    ("kivi_k2v2", lambda k: k.LayerSpec.kivi(2, 2)),
+    ("kivi_k2v8", lambda k: k.LayerSpec.kivi(2, 8)),
+    ("kivi_k8v2", lambda k: k.LayerSpec.kivi(8, 2)),
     ("kivi_k2v4_r64", lambda k: k.LayerSpec.kivi(2, 4, residual=64)),
     ("kivi_k8v4_g64", lambda k: k.LayerSpec.kivi(8, 4, group=64, residual=64)),
     ("kivi_k16v4", lambda k: k.LayerSpec.kivi(16, 4)),

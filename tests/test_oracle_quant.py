@@ -213,3 +213,25 @@ def test_o2_meta_is_16_bytes_per_token(oracle):
         sz = oracle.slice_bytes(mode, 4, 2, 32, 32, 128, 8192)
         assert sz[1] == 8192 * 16 and sz[4] == 8192 * 16
         assert sz[0] == 8192 * 64 and sz[3] == 8192 * 32
+
+
+@pytest.mark.parametrize("vb", [2, 4, 8])
+def test_o2_blocked_value_layout_is_a_block_permutation(oracle, vb):
+    """KIVI value codes (G = 32, quantised K and V) use the blocked layout — within each
+    complete 32-token block it is a permutation of the token-major rows the per-token mode stores for
+    the same (per-token, G = 32) Eq. 2 groups; every byte of a complete block is defined."""
+    d, S = 128, 100
+    K = kvt_synth.bf16_bits(kvt_synth.keys((S, d), seed=vb))
+    V = kvt_synth.bf16_bits(kvt_synth.values((S, d), seed=vb + 1))
+    kivi = oracle.defined_bytes(1, 4, vb, 32, 32, d, 128, K, V)["v_codes"]
+    tm = oracle.defined_bytes(0, 4, vb, 32, 32, d, 128, K, V)["v_codes"]     # per-token, window 32: same V tokens
+    rb = d * vb // 8
+    nqv = oracle.n_quantized_value(1, vb, 32, 32, S)                          # 68 → two complete blocks
+    for blk in range(nqv // 32):
+        a = kivi[0][blk * 32 * rb:(blk + 1) * 32 * rb]
+        m = kivi[1][blk * 32 * rb:(blk + 1) * 32 * rb]
+        b = tm[0][blk * 32 * rb:(blk + 1) * 32 * rb]
+        assert m.all()
+        assert np.array_equal(np.sort(a), np.sort(b))
+        assert not np.array_equal(a, b)                                       # it is not the identity
+    assert int(kivi[1].sum()) == nqv * rb
