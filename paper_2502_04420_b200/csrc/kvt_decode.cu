@@ -7,6 +7,9 @@
 
 #include "kvt_decode.cuh"
 
+#if KVT_TRACE
+static unsigned long long* g_trace = nullptr;
+#endif
 namespace kvt {
 namespace dec {
 using KFn = void (*)(DecodeArgs);
@@ -149,12 +152,31 @@ static int kernel_kind(const Geometry& g) {
 
 static size_t parts_bytes(int ns, int B, int H_q) { return ((size_t)ns * B * H_q * (dec::D + 2) * sizeof(float) + 255) & ~(size_t)255; }
 static size_t counters_bytes(const Geometry& g) { return ((size_t)g.B * g.H * sizeof(int) + 255) & ~(size_t)255; }
+// stream-K partial slots of the tensor-core kernel: [n_cta][2][8 heads][D + 2]
+static size_t sk_parts_bytes(int n_cta) { return ((size_t)n_cta * 2 * 8 * (dec::D + 2) * sizeof(float) + 255) & ~(size_t)255; }
+
+// Stream-K CTAs (tensor-core kernel): at most one wave of resident CTAs (estimated from plan_len; the kernel
+// clamps to the actual total work).
+static int plan_ctas(const Geometry& g, int plan_len, int occ, int sms) {
+    static const int forced = [] { const char* e = getenv("KVT_NCTA"); return e ? atoi(e) : 0; }();
+    if (forced > 0) return forced;                      // experiments only
+    const long long units = (long long)g.B * g.H;
+    const long long C = units * dec::unit_cost(g, plan_len).cost;
+    long long n = (C + 15) / 16;                        // cut units only into pieces of >= ~16 work units
+    if (n < units) n = units;                           // ... but never leave whole units waiting in line
+    if (n > (long long)occ * sms) n = (long long)occ * sms;
+    return n < 1 ? 1 : (int)n;
+}
 
 size_t decode_workspace(const Geometry& g, int H_q, int plan_len) {
     using namespace dec;
     int GM = (H_q / g.H) <= 4 ? 4 : 8;
     Instance in; int sms = 148;
     if (get_instance(g.kb, g.vb, kernel_kind(g), GM, &in, &sms) != KVT_OK) { in.occ = 4; sms = 148; }
+    if (kernel_kind(g) == 2) {
+        const int n = plan_ctas(g, plan_len, in.occ, sms);
+        return n > 1 ? sk_parts_bytes(n) + counters_bytes(g) : 0;
+    }
     int ns = plan_splits(g, plan_len, in.occ, sms);
     return ns > 1 ? parts_bytes(ns, g.B, H_q) + counters_bytes(g) : 0;
 }
@@ -168,29 +190,49 @@ int32_t launch_decode(const Geometry& g, const CachePtrs& c, const uint16_t* q, 
     Instance in; int sms = 148;
     int32_t st = get_instance(g.kb, g.vb, kernel_kind(g), GM, &in, &sms);
     if (st) return st;
-    int ns = plan_splits(g, plan_len, in.occ, sms);
     const int kind = kernel_kind(g);
-    size_t need = ns > 1 ? parts_bytes(ns, g.B, H_q) + counters_bytes(g) : 0;
-    if (need > ws_bytes || (need && !workspace))
-        return fail(KVT_ERR_WORKSPACE, "decode: workspace %zu < %zu bytes (use kvt_decode_workspace_bytes)", ws_bytes, need);
     if (g.B > 65535 || g.H > 65535) return fail(KVT_ERR_UNSUPPORTED, "decode: batch/heads exceed grid limits");
     DecodeArgs a;
     a.g = g; a.c = c; a.q = q; a.H_q = H_q; a.gq = gq; a.seq_len = seq_len;
     a.scale_log2 = scale * 1.4426950408889634f;
     a.out = out;
+    a.final_mode = out_mode;
+    if (kind == 2) {
+        // tensor-core kernel: stream-K over all (b, kv head) units, fused merge of units cut across CTAs
+        const int n = plan_ctas(g, plan_len, in.occ, sms);
+        const size_t need = n > 1 ? sk_parts_bytes(n) + counters_bytes(g) : 0;
+        if (need > ws_bytes || (need && !workspace))
+            return fail(KVT_ERR_WORKSPACE, "decode: workspace %zu < %zu bytes (use kvt_decode_workspace_bytes)", ws_bytes, need);
+        a.out_mode = out_mode;
+        a.parts = (float*)workspace;
+        a.counters = n > 1 ? (int*)((char*)workspace + sk_parts_bytes(n)) : nullptr;
+        a.n_split = 1;
+        a.n_cta = n;
+        a.trace = nullptr;
+#if KVT_TRACE
+        if (!g_trace) cudaMalloc(&g_trace, sizeof(unsigned long long) * 3 * 4096);
+        a.trace = g_trace;
+#endif
+        in.fn<<<n, kThreads, in.smem, (cudaStream_t)stream>>>(a);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return fail(KVT_ERR_CUDA, "decode launch: %s", cudaGetErrorString(e));
+        return KVT_OK;
+    }
+    int ns = plan_splits(g, plan_len, in.occ, sms);
+    size_t need = ns > 1 ? parts_bytes(ns, g.B, H_q) + counters_bytes(g) : 0;
+    if (need > ws_bytes || (need && !workspace))
+        return fail(KVT_ERR_WORKSPACE, "decode: workspace %zu < %zu bytes (use kvt_decode_workspace_bytes)", ws_bytes, need);
     a.out_mode = ns > 1 ? 3 : out_mode;
     a.parts = (float*)workspace;
     a.n_split = ns;
-    // tensor-core kernel: the last CTA per (b, kv head) merges the splits (workspace counters, zero between
-    // calls); the generic kernel uses the separate combine launch
-    const bool fused = (ns > 1) && (kind == 2);
-    a.counters = fused ? (int*)((char*)workspace + parts_bytes(ns, g.B, H_q)) : nullptr;
-    a.final_mode = out_mode;
+    a.counters = nullptr;      // the generic kernel merges its splits with the separate combine launch
+    a.n_cta = 0;
+    a.trace = nullptr;
     dim3 grid(ns, g.H, g.B);
     in.fn<<<grid, kThreads, in.smem, (cudaStream_t)stream>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(KVT_ERR_CUDA, "decode launch: %s", cudaGetErrorString(e));
-    if (ns > 1 && !fused) {
+    if (ns > 1) {
         int rows = g.B * H_q;
         combine_kernel<<<(rows + 3) / 4, 128, 0, (cudaStream_t)stream>>>((const float*)workspace, ns, rows, out, out_mode);
         e = cudaGetLastError();
@@ -210,3 +252,9 @@ int32_t launch_combine(const float* parts, int n_parts, int B, int H_q, int d, v
 }
 
 }  // namespace kvt
+
+#if KVT_TRACE
+extern "C" int32_t kvt_debug_trace(unsigned long long* host, int32_t n) {
+    return g_trace && cudaMemcpy(host, g_trace, sizeof(unsigned long long) * 3 * (size_t)n, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 8;
+}
+#endif

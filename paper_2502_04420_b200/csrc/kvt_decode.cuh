@@ -54,7 +54,24 @@ struct DecodeArgs {
     int n_split;
     int* counters;     // [B][H_kv] split-arrival counters (fused combine), zero between calls; or null
     int final_mode;    // output mode of the fused combine (0, 1 or 2)
+    unsigned long long* trace;   // KVT_TRACE builds only: per-CTA (SM, start, end); else null
+    int n_cta;         // tensor-core kernel: stream-K CTAs (parts [n_cta][2][8][D + 2], counters [B][H_kv])
 };
+
+// Stream-K cost of one (b, kv head) unit of the tensor-core kernel (kvt_decode_mma.cuh)
+struct UnitCost {
+    int n_main, tiles, cost;
+};
+__host__ __device__ inline UnitCost unit_cost(const Geometry& g, int S) {
+    const int nqK = nq_key(g.mode, g.kb, g.G, g.R, S);
+    const int nqV = nq_per_token(g.vb, g.R, S);
+    UnitCost u;
+    u.n_main = ((nqK < nqV ? nqK : nqV) / 32) * 32;
+    u.tiles = u.n_main / 32;
+    u.cost = u.tiles + (S - u.n_main + 7) / 8;
+    if (u.cost < 1) u.cost = 1;
+    return u;
+}
 
 __device__ __forceinline__ float bf2f(uint32_t b16) { return __uint_as_float(b16 << 16); }
 

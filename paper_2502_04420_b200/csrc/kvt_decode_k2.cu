@@ -29,9 +29,9 @@ KFn get_decode_k2(int VB, bool KPC, int GM) {
 // tensor-core KIVI instances (G = 32): returns the kernel and its dynamic shared memory
 KFn get_decode_mma_k2(int VB, int GM, size_t* smem) {
     switch (VB) {
-        case 2: *smem = mma::Geo<2, 2>::SMEM; return GM == 4 ? mma::decode_mma_kernel<2, 2, 4> : mma::decode_mma_kernel<2, 2, 8>;
-        case 4: *smem = mma::Geo<2, 4>::SMEM; return GM == 4 ? mma::decode_mma_kernel<2, 4, 4> : mma::decode_mma_kernel<2, 4, 8>;
-        default: *smem = mma::Geo<2, 8>::SMEM; return GM == 4 ? mma::decode_mma_kernel<2, 8, 4> : mma::decode_mma_kernel<2, 8, 8>;
+        case 2: *smem = GM == 4 ? mma::Geo<2, 2, 4>::SMEM : mma::Geo<2, 2, 8>::SMEM; return GM == 4 ? mma::decode_mma_kernel<2, 2, 4> : mma::decode_mma_kernel<2, 2, 8>;
+        case 4: *smem = GM == 4 ? mma::Geo<2, 4, 4>::SMEM : mma::Geo<2, 4, 8>::SMEM; return GM == 4 ? mma::decode_mma_kernel<2, 4, 4> : mma::decode_mma_kernel<2, 4, 8>;
+        default: *smem = GM == 4 ? mma::Geo<2, 8, 4>::SMEM : mma::Geo<2, 8, 8>::SMEM; return GM == 4 ? mma::decode_mma_kernel<2, 8, 4> : mma::decode_mma_kernel<2, 8, 8>;
     }
 }
 

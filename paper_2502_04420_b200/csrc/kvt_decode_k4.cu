@@ -29,9 +29,9 @@ KFn get_decode_k4(int VB, bool KPC, int GM) {
 // tensor-core KIVI instances (G = 32): returns the kernel and its dynamic shared memory
 KFn get_decode_mma_k4(int VB, int GM, size_t* smem) {
     switch (VB) {
-        case 2: *smem = mma::Geo<4, 2>::SMEM; return GM == 4 ? mma::decode_mma_kernel<4, 2, 4> : mma::decode_mma_kernel<4, 2, 8>;
-        case 4: *smem = mma::Geo<4, 4>::SMEM; return GM == 4 ? mma::decode_mma_kernel<4, 4, 4> : mma::decode_mma_kernel<4, 4, 8>;
-        default: *smem = mma::Geo<4, 8>::SMEM; return GM == 4 ? mma::decode_mma_kernel<4, 8, 4> : mma::decode_mma_kernel<4, 8, 8>;
+        case 2: *smem = GM == 4 ? mma::Geo<4, 2, 4>::SMEM : mma::Geo<4, 2, 8>::SMEM; return GM == 4 ? mma::decode_mma_kernel<4, 2, 4> : mma::decode_mma_kernel<4, 2, 8>;
+        case 4: *smem = GM == 4 ? mma::Geo<4, 4, 4>::SMEM : mma::Geo<4, 4, 8>::SMEM; return GM == 4 ? mma::decode_mma_kernel<4, 4, 4> : mma::decode_mma_kernel<4, 4, 8>;
+        default: *smem = GM == 4 ? mma::Geo<4, 8, 4>::SMEM : mma::Geo<4, 8, 8>::SMEM; return GM == 4 ? mma::decode_mma_kernel<4, 8, 4> : mma::decode_mma_kernel<4, 8, 8>;
     }
 }
 

@@ -35,6 +35,8 @@ using dec::DecodeArgs;
 using dec::Slice;
 using dec::bf2f;
 using dec::kFull;
+using dec::UnitCost;
+using dec::unit_cost;
 constexpr int D = 128;
 constexpr int kTile = 32;
 constexpr int kWarps = 4;
@@ -71,6 +73,15 @@ __device__ __forceinline__ Mul make_mul() {
 #ifndef KVT_MINB
 #define KVT_MINB 4
 #endif
+#ifndef KVT_FIXK
+#define KVT_FIXK 0     // 1: no per-block key-scale exponent (q scaled to <= 2^3 instead)
+#endif
+#ifndef KVT_TAILN
+#define KVT_TAILN 4    // tail tokens per warp iteration (loads batched ahead of the math)
+#endif
+#ifndef KVT_TRACE
+#define KVT_TRACE 0    // debug builds only: per-CTA (SM, start, end) timestamps for load-balance studies
+#endif
 #ifndef KVT_EXP
 #define KVT_EXP 0      // profiling experiments only: 1 = skip PV, 2 = skip QK
 #endif
@@ -93,6 +104,13 @@ __device__ __forceinline__ uint32_t pack16(uint32_t lo, uint32_t hi, const Mul& 
 #endif
 }
 
+// 2^x on the SFU (MUFU.EX2, flush-to-zero). exp2f adds a subnormal range fix-up (~4 more instructions) that
+// softmax does not need: every argument here is <= 8 and results below 2^-126 are negligible against l >= 1.
+__device__ __forceinline__ float fexp2(float x) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
 __device__ __forceinline__ int frexp_e(float x) {           // x = f 2^e, f in [0.5, 1); clamped
     const int e = x > 0.0f ? (int)((__float_as_uint(x) >> 23) & 0xFF) - 126 : 0;
     return e < -90 ? -90 : (e > 90 ? 90 : e);
@@ -207,7 +225,7 @@ __device__ __forceinline__ void write_row(void* out, int mode, size_t row, int c
     }
 }
 
-template <int KB, int VB>
+template <int KB, int VB, int GM>
 struct Geo {
     static constexpr int KROW = 16 * KB;                 // bytes per key code row
     static constexpr int VROW = 16 * VB;
@@ -226,10 +244,14 @@ struct Geo {
     static constexpr int SH_OFF = W_OFF + W_BYTES;
     static constexpr int BAR_OFF = SH_OFF + 4 * 16 * 4;           // one mbarrier per stage
     static constexpr int WARP_BYTES = BAR_OFF + 8 * NS;
-    static constexpr int Q_BYTES = 8 * D * 4;            // q fp32 [8][128]
-    static constexpr int COMB_BYTES = 2 * kWarps * 8 * (2 + D) * 4;
-    static constexpr int BODY = kWarps * WARP_BYTES > COMB_BYTES ? kWarps * WARP_BYTES : COMB_BYTES;
-    static constexpr size_t SMEM = (size_t)Q_BYTES + BODY;
+    static constexpr int Q_BYTES = GM * D * 4;           // q fp32 [GM][128]
+    static constexpr int TAIL_PART = ((GM * (2 + D) * 4) + 15) / 16 * 16;    // tail partial (m, l, o) [GM]
+    static constexpr int TAIL_BYTES = TAIL_PART + 16;                          // + the tail-staging mbarrier
+    static constexpr int COMB_BYTES = kWarps * 8 * (2 + D) * 4;
+    static constexpr int SCRATCH_BYTES = kWarps * GM * (2 + D) * 4;       // per-warp tail partials
+    static constexpr int BODY0 = kWarps * WARP_BYTES > COMB_BYTES ? kWarps * WARP_BYTES : COMB_BYTES;
+    static constexpr int BODY = BODY0 > SCRATCH_BYTES ? BODY0 : SCRATCH_BYTES;
+    static constexpr size_t SMEM = (size_t)Q_BYTES + TAIL_BYTES + BODY;
 };
 
 // ---- TMA bulk copies (cp.async.bulk) completing on a per-stage mbarrier ----
@@ -261,15 +283,19 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+// One segment of a (b, kv head) unit: main tiles [tile_lo, tile_hi) (+ the tail tokens [n_main, S) when
+// do_tail).  count == 1: the segment is the whole unit and writes the output row; otherwise it leaves a
+// partial in parts slot (cta, slot) and the last of the unit's `count` CTAs (c_first ...) merges them.
 // GM: 4 (g <= 4: n = 4 heads x {hi, lo}) or 8 (g <= 8: separate hi and lo MMAs).
 template <int KB, int VB, int GM>
-__global__ void __launch_bounds__(kThreads, GM == 4 ? KVT_MINB : 3) decode_mma_kernel(DecodeArgs a) {
-    using Gm = Geo<KB, VB>;
-    extern __shared__ __align__(16) uint8_t smem[];
-    float* q_s = reinterpret_cast<float*>(smem);                           // [8][128]
-    uint8_t* body = smem + Gm::Q_BYTES;
+__device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, const int b, const int hk,
+                                        const int tile_lo, const int tile_hi, const bool do_tail, const int cta,
+                                        const int slot, const int c_first, const int count) {
+    using Gm = Geo<KB, VB, GM>;
+    float* q_s = reinterpret_cast<float*>(smem);                           // [GM][128]
+    float* tail_s = reinterpret_cast<float*>(smem + Gm::Q_BYTES);          // [GM][2 + D]
+    uint8_t* body = smem + Gm::Q_BYTES + Gm::TAIL_BYTES;
     const Geometry& g = a.g;
-    const int split = blockIdx.x, hk = blockIdx.y, b = blockIdx.z;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int gid = lane >> 2, tig = lane & 3;
     const int gq = a.gq;
@@ -281,7 +307,7 @@ __global__ void __launch_bounds__(kThreads, GM == 4 ? KVT_MINB : 3) decode_mma_k
 
     {   // q -> shared fp32 (zero for padded heads)
         const uint16_t* qg = a.q + ((size_t)b * a.H_q + (size_t)hk * gq) * D;
-        for (int h = 0; h < 8; ++h) q_s[h * D + tid] = (h < gq && h < GM) ? bf2f(qg[(size_t)h * D + tid]) : 0.0f;
+        for (int h = 0; h < GM; ++h) q_s[h * D + tid] = h < gq ? bf2f(qg[(size_t)h * D + tid]) : 0.0f;
     }
     for (int i = lane; i < Gm::W_BYTES / 4; i += 32) w_s[i] = 0u;
     __syncthreads();
@@ -298,19 +324,55 @@ __global__ void __launch_bounds__(kThreads, GM == 4 ? KVT_MINB : 3) decode_mma_k
     const int nqK = nq_key(g.mode, g.kb, g.G, g.R, S);
     const int nqV = nq_per_token(g.vb, g.R, S);
     const int n_main = ((nqK < nqV ? nqK : nqV) / kTile) * kTile;
-    const int n_tiles = n_main / kTile;
-    const int tps = (n_tiles + a.n_split - 1) / a.n_split;
-    const int tile_lo = split * tps;
-    const int tile_hi = (tile_lo + tps < n_tiles) ? tile_lo + tps : n_tiles;
     const int n_my = tile_hi - tile_lo - warp > 0 ? (tile_hi - tile_lo - warp + kWarps - 1) / kWarps : 0;
+    // ---- stage the tail rows [n_main, S) into shared memory with bulk copies (one round trip instead of a
+    // dependent global load per token group); `tl` then addresses them with the cache's own indexing ----
+    Slice tl = sl;
+    uint64_t* tbar = reinterpret_cast<uint64_t*>(smem + Gm::Q_BYTES + Gm::TAIL_PART);
+    bool staged = false;
+    if (KVT_EXP != 5 && do_tail && n_main < S) {
+        const int kq = nqK < S ? nqK : S, vq = nqV < S ? nqV : S;
+        const uint32_t b_kc = (uint32_t)(kq - n_main) * Gm::KROW;
+        const uint32_t b_km = (uint32_t)((kq - n_main + kTile - 1) / kTile) * D * 4;
+        const uint32_t b_kr = (uint32_t)(S - kq) * D * 2;
+        const uint32_t b_vc = vq > n_main ? (uint32_t)kTile * Gm::VROW : 0u;
+        const uint32_t b_vm = (uint32_t)(vq - n_main) * 16;
+        const uint32_t b_vr = (vq < S && sl.vr) ? (uint32_t)g.R * D * 2 : 0u;
+        const uint32_t total = b_kc + b_km + b_kr + b_vc + b_vm + b_vr;   // all multiples of 16
+        if (Gm::SCRATCH_BYTES + total <= (uint32_t)Gm::BODY) {
+            staged = true;
+            uint8_t* p = body + Gm::SCRATCH_BYTES;
+            uint8_t* p_kc = p;           uint8_t* p_km = p_kc + b_kc; uint8_t* p_kr = p_km + b_km;
+            uint8_t* p_vc = p_kr + b_kr; uint8_t* p_vm = p_vc + b_vc; uint8_t* p_vr = p_vm + b_vm;
+            if (tid == 0) {
+                mbar_init(tbar);
+                asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+                fence_proxy_async();
+                mbar_expect_tx(tbar, total);
+                if (b_kc) bulk_g2s(p_kc, sl.kc + (size_t)n_main * Gm::KROW, b_kc, tbar);
+                if (b_km) bulk_g2s(p_km, sl.km + (size_t)(n_main / kTile) * D, b_km, tbar);
+                if (b_kr) bulk_g2s(p_kr, sl.kr, b_kr, tbar);
+                if (b_vc) bulk_g2s(p_vc, sl.vc + (size_t)n_main * Gm::VROW, b_vc, tbar);
+                if (b_vm) bulk_g2s(p_vm, sl.vm + (size_t)n_main * 4, b_vm, tbar);
+                if (b_vr) bulk_g2s(p_vr, sl.vr, b_vr, tbar);
+            }
+            // virtual bases: row t of the cache lands at its staged copy under the cache's own indexing
+            tl.kc = p_kc - (size_t)n_main * Gm::KROW;
+            tl.km = reinterpret_cast<const uint32_t*>(p_km) - (size_t)(n_main / kTile) * D;
+            tl.kr = reinterpret_cast<const uint16_t*>(p_kr);
+            tl.vc = p_vc - (size_t)n_main * Gm::VROW;
+            tl.vm = reinterpret_cast<const uint32_t*>(p_vm) - (size_t)n_main * 4;
+            tl.vr = reinterpret_cast<const uint16_t*>(p_vr);
+        }
+    }
 
     // softmax heads of this thread (the QK D columns it holds after the hi/lo fold)
     const int hA = (GM == 8) ? 2 * tig : 2 * (tig & 1);
     // ---- per-head power-of-two scale of q (max |q 2^qa| in [64, 128)), computed once per CTA ----
-    float* qmax_s = reinterpret_cast<float*>(body) + 0;   // body is free until the ring is first used
+    float* qmax_s = tail_s;                               // tail_s is free until the tail is merged
     if (warp == 0) {
 #pragma unroll
-        for (int h = 0; h < 8; ++h) {
+        for (int h = 0; h < GM; ++h) {
             const float4 v = *reinterpret_cast<const float4*>(q_s + h * D + 4 * lane);
             float m = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
 #pragma unroll
@@ -323,7 +385,7 @@ __global__ void __launch_bounds__(kThreads, GM == 4 ? KVT_MINB : 3) decode_mma_k
     float qa_inv[2];
     {
         const int qh = (GM == 4) ? (gid & 3) : gid;
-        const int qa = 7 - frexp_e(qmax_s[qh]);
+        const int qa = (KVT_FIXK ? 3 : 7) - frexp_e(qmax_s[qh]);
 #pragma unroll
         for (int m = 0; m < 16; ++m) {
             const float sc = pow2(qa - KSlots<KB>::P(m));
@@ -331,7 +393,7 @@ __global__ void __launch_bounds__(kThreads, GM == 4 ? KVT_MINB : 3) decode_mma_k
                                            q_s[qh * D + 32 * tig + KSlots<KB>::c1(m)] * sc));
         }
 #pragma unroll
-        for (int j = 0; j < 2; ++j) qa_inv[j] = pow2(24 - (7 - frexp_e(qmax_s[hA + j])));   // undoes 2^qa, 2^-24
+        for (int j = 0; j < 2; ++j) qa_inv[j] = pow2(24 - ((KVT_FIXK ? 3 : 7) - frexp_e(qmax_s[hA + j])));   // undoes 2^qa, 2^-24
     }
     __syncthreads();
     // GM == 4: lanes tig and tig^2 hold the same probabilities, so they prepare different value groups:
@@ -351,6 +413,98 @@ __global__ void __launch_bounds__(kThreads, GM == 4 ? KVT_MINB : 3) decode_mma_k
     for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.0f;
     int kp = 126;                  // PV weight exponent (only decreases)
 
+    // ---- tail tokens [n_main, S) first: token at a time, lane = channels [4 lane, 4 lane + 4).  Run before
+    // the main loop (its dependent global loads would otherwise sit at the end of the CTA, when the whole
+    // wave ends together and memory latency is at its worst); per-warp partials go to scratch in the ring
+    // area, which the TMA ring only uses afterwards, and are merged into tail_s. ----
+    {
+        float* cw = reinterpret_cast<float*>(body) + warp * GM * (2 + D);
+        float mt_[GM], lt[GM], ot[GM][4];
+#pragma unroll
+        for (int h = 0; h < GM; ++h) {
+            mt_[h] = -INFINITY; lt[h] = 0.0f;
+            ot[h][0] = ot[h][1] = ot[h][2] = ot[h][3] = 0.0f;
+        }
+        if (staged) mbar_wait(tbar, 0);
+        if (KVT_EXP != 5 && do_tail) {
+            // KVT_TAILN tokens per iteration: all loads first, then four independent dot/shuffle chains
+            for (int t0 = n_main + warp; t0 < S; t0 += KVT_TAILN * kWarps) {
+                float kx[KVT_TAILN][4], vx[KVT_TAILN][4];
+#pragma unroll
+                for (int u = 0; u < KVT_TAILN; ++u) {
+                    const int t = t0 + u * kWarps;
+                    if (t < S) {
+                        dec::tail_k<KB, true>(tl, g, t, nqK, lane, kx[u]);
+                        dec::tail_v<VB, true>(tl, g, t, nqV, lane, vx[u]);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) kx[u][i] = vx[u][i] = 0.0f;
+                    }
+                }
+                float sc[KVT_TAILN][GM];
+#pragma unroll
+                for (int h = 0; h < GM; ++h) {
+                    const float4 qv = *reinterpret_cast<const float4*>(q_s + h * D + 4 * lane);
+#pragma unroll
+                    for (int u = 0; u < KVT_TAILN; ++u)
+                        sc[u][h] = qv.x * kx[u][0] + qv.y * kx[u][1] + qv.z * kx[u][2] + qv.w * kx[u][3];
+                }
+#pragma unroll
+                for (int off = 16; off >= 1; off >>= 1)
+#pragma unroll
+                    for (int u = 0; u < KVT_TAILN; ++u)
+#pragma unroll
+                        for (int h = 0; h < GM; ++h) sc[u][h] += __shfl_xor_sync(kFull, sc[u][h], off);
+#pragma unroll
+                for (int u = 0; u < KVT_TAILN; ++u) {
+                    if (t0 + u * kWarps >= S) break;
+#pragma unroll
+                    for (int h = 0; h < GM; ++h) {
+                        const float sv = sc[u][h] * a.scale_log2;
+                        const float mn = fmaxf(mt_[h], sv);
+                        const float al = fexp2(mt_[h] - mn);
+                        const float pp = fexp2(sv - mn);
+                        lt[h] = lt[h] * al + pp;
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) ot[h][i] = ot[h][i] * al + pp * vx[u][i];
+                        mt_[h] = mn;
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int h = 0; h < GM; ++h) {
+            float* ch = cw + h * (2 + D);
+            if (lane == 0) { ch[0] = mt_[h]; ch[1] = lt[h]; }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) ch[2 + 4 * lane + i] = ot[h][i];
+        }
+    }
+    __syncthreads();
+    {   // merge the warps' tail partials: thread = channel
+        const int c = tid;
+        const float* sc = reinterpret_cast<const float*>(body);
+        for (int h = 0; h < GM; ++h) {
+            float M = -INFINITY, L = 0.0f, O = 0.0f;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) M = fmaxf(M, sc[(w * GM + h) * (2 + D)]);
+            if (M != -INFINITY) {
+#pragma unroll
+                for (int w = 0; w < kWarps; ++w) {
+                    const float* cw = sc + (w * GM + h) * (2 + D);
+                    if (cw[1] == 0.0f) continue;
+                    const float scl = fexp2(cw[0] - M);
+                    L += cw[1] * scl;
+                    O += cw[2 + c] * scl;
+                }
+            }
+            float* th = tail_s + h * (2 + D);
+            if (c == 0) { th[0] = M; th[1] = L; }
+            th[2 + c] = O;
+        }
+    }
+    if (staged && tid == 0) asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(tbar)));
+    __syncthreads();
     // ---- per-warp TMA ring: lane 0 issues four bulk copies per tile onto the stage's mbarrier ----
     uint64_t* bars = reinterpret_cast<uint64_t*>(wbase + Gm::BAR_OFF);
     if (lane == 0) {
@@ -393,11 +547,15 @@ __global__ void __launch_bounds__(kThreads, GM == 4 ? KVT_MINB : 3) decode_mma_k
         {
             const uint4 m4 = reinterpret_cast<const uint4*>(km_s)[lane];
             const uint32_t mw[4] = {m4.x, m4.y, m4.z, m4.w};
+#if KVT_FIXK
+            const int sbx = 0;
+#else
             // the largest scale: positive bf16 bit patterns order like their values
             uint32_t smb = max(max(mw[0] & 0xffffu, mw[1] & 0xffffu), max(mw[2] & 0xffffu, mw[3] & 0xffffu));
 #pragma unroll
             for (int off = 16; off >= 1; off >>= 1) smb = max(smb, __shfl_xor_sync(kFull, smb, off));
             const int sbx = 7 - frexp_e(bf2f(smb));
+#endif
             const float ssc = pow2(sbx);
             ks_inv = pow2(-sbx);
             __half* shh = reinterpret_cast<__half*>(sh_s);
@@ -536,15 +694,15 @@ __global__ void __launch_bounds__(kThreads, GM == 4 ? KVT_MINB : 3) decode_mma_k
             mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 16));
             alpha[j] = 1.0f;
             if (mx > m_run[j] + 8.0f) {
-                alpha[j] = exp2f(m_run[j] - mx);
+                alpha[j] = fexp2(m_run[j] - mx);
                 m_run[j] = mx;
                 resc = true;
             }
             const float mr = m_run[j];
-            p[0][0][j] = exp2f(l4[0] - mr);
-            p[0][1][j] = exp2f(l4[1] - mr);
-            p[1][0][j] = exp2f(l4[2] - mr);
-            p[1][1][j] = exp2f(l4[3] - mr);
+            p[0][0][j] = fexp2(l4[0] - mr);
+            p[0][1][j] = fexp2(l4[1] - mr);
+            p[1][0][j] = fexp2(l4[2] - mr);
+            p[1][1][j] = fexp2(l4[3] - mr);
             l_part[j] = l_part[j] * alpha[j] + ((p[0][0][j] + p[0][1][j]) + (p[1][0][j] + p[1][1][j]));
         }
         // (5) value weights w = p * s_v * 2^kp (fp16 pairs (T, T+8)) and zero sums p * z_v
@@ -683,104 +841,41 @@ __global__ void __launch_bounds__(kThreads, GM == 4 ? KVT_MINB : 3) decode_mma_k
             }
         }
     }
-    // ---- tail tokens [n_main, S) (last split): token at a time, lane = channels [4 lane, 4 lane + 4) ----
-    {
-        float* cw = comb + (kWarps + warp) * 8 * (2 + D);
-        float mt_[GM], lt[GM], ot[GM][4];
-#pragma unroll
-        for (int h = 0; h < GM; ++h) {
-            mt_[h] = -INFINITY; lt[h] = 0.0f;
-            ot[h][0] = ot[h][1] = ot[h][2] = ot[h][3] = 0.0f;
-        }
-        if (split == a.n_split - 1) {
-            // four tokens per iteration: all loads first, then four independent dot/shuffle chains
-            for (int t0 = n_main + warp; t0 < S; t0 += 4 * kWarps) {
-                float kx[4][4], vx[4][4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int t = t0 + u * kWarps;
-                    if (t < S) {
-                        dec::tail_k<KB, true>(sl, g, t, nqK, lane, kx[u]);
-                        dec::tail_v<VB, true>(sl, g, t, nqV, lane, vx[u]);
-                    } else {
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) kx[u][i] = vx[u][i] = 0.0f;
-                    }
-                }
-                float sc[4][GM];
-#pragma unroll
-                for (int h = 0; h < GM; ++h) {
-                    const float4 qv = *reinterpret_cast<const float4*>(q_s + h * D + 4 * lane);
-#pragma unroll
-                    for (int u = 0; u < 4; ++u)
-                        sc[u][h] = qv.x * kx[u][0] + qv.y * kx[u][1] + qv.z * kx[u][2] + qv.w * kx[u][3];
-                }
-#pragma unroll
-                for (int off = 16; off >= 1; off >>= 1)
-#pragma unroll
-                    for (int u = 0; u < 4; ++u)
-#pragma unroll
-                        for (int h = 0; h < GM; ++h) sc[u][h] += __shfl_xor_sync(kFull, sc[u][h], off);
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    if (t0 + u * kWarps >= S) break;
-#pragma unroll
-                    for (int h = 0; h < GM; ++h) {
-                        const float sv = sc[u][h] * a.scale_log2;
-                        const float mn = fmaxf(mt_[h], sv);
-                        const float al = exp2f(mt_[h] - mn);
-                        const float pp = exp2f(sv - mn);
-                        lt[h] = lt[h] * al + pp;
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) ot[h][i] = ot[h][i] * al + pp * vx[u][i];
-                        mt_[h] = mn;
-                    }
-                }
-            }
-        }
-#pragma unroll
-        for (int h = 0; h < GM; ++h) {
-            float* ch = cw + h * (2 + D);
-            if (lane == 0) { ch[0] = mt_[h]; ch[1] = lt[h]; }
-#pragma unroll
-            for (int i = 0; i < 4; ++i) ch[2 + 4 * lane + i] = ot[h][i];
-        }
-    }
     __syncthreads();
-    // ---- CTA combine of the 8 partials: thread = channel ----
+    // ---- CTA combine of the warps' partials and the tail partial: thread = channel ----
     const int c = tid;
     for (int h = 0; h < gq; ++h) {
-        float M = -INFINITY;
+        float M = tail_s[h * (2 + D)];
 #pragma unroll
-        for (int w = 0; w < 2 * kWarps; ++w) M = fmaxf(M, comb[(w * 8 + h) * (2 + D)]);
+        for (int w = 0; w < kWarps; ++w) M = fmaxf(M, comb[(w * 8 + h) * (2 + D)]);
         float L = 0.0f, O = 0.0f;
         if (M != -INFINITY) {
 #pragma unroll
-            for (int w = 0; w < 2 * kWarps; ++w) {
-                const float* cw = comb + (w * 8 + h) * (2 + D);
+            for (int w = 0; w <= kWarps; ++w) {
+                const float* cw = w < kWarps ? comb + (w * 8 + h) * (2 + D) : tail_s + h * (2 + D);
                 if (cw[1] == 0.0f) continue;
-                const float scl = exp2f(cw[0] - M);
+                const float scl = fexp2(cw[0] - M);
                 L += cw[1] * scl;
                 O += cw[2 + c] * scl;
             }
         }
         const size_t row = (size_t)b * a.H_q + (size_t)hk * gq + h;
-        if (a.out_mode == 3) {
-            float* pr = a.parts + ((size_t)split * g.B * a.H_q + row) * (2 + D);
+        if (count == 1) {
+            write_row(a.out, a.out_mode, row, c, M, L, O);
+        } else {
+            float* pr = a.parts + ((size_t)(cta * 2 + slot) * 8 + h) * (2 + D);
             if (c == 0) { pr[0] = M; pr[1] = L; }
             pr[2 + c] = L > 0.0f ? __fdiv_rn(O, L) : 0.0f;
-        } else {
-            write_row(a.out, a.out_mode, row, c, M, L, O);
         }
     }
-    // ---- fused split combine (K3): the last CTA of this (b, kv head) to arrive merges the partials ----
-    if (a.out_mode == 3 && a.counters != nullptr) {
+    // ---- fused combine (K3): the last of the unit's CTAs to arrive merges its partials ----
+    if (count > 1) {
         __shared__ int is_last;
         __threadfence();                      // every thread's partial writes are visible device-wide ...
-        __syncthreads();                      // ... before thread 0 announces this split
+        __syncthreads();                      // ... before thread 0 announces this segment
         if (tid == 0) {
             const int old = atomicAdd(a.counters + bh, 1);
-            is_last = (old == a.n_split - 1);
+            is_last = (old == count - 1);
         }
         __syncthreads();
         if (is_last) {
@@ -788,24 +883,103 @@ __global__ void __launch_bounds__(kThreads, GM == 4 ? KVT_MINB : 3) decode_mma_k
             for (int h = 0; h < gq; ++h) {
                 const size_t row = (size_t)b * a.H_q + (size_t)hk * gq + h;
                 float M = -INFINITY;
-                for (int sp = 0; sp < a.n_split; ++sp)
-                    M = fmaxf(M, __ldcg(a.parts + ((size_t)sp * g.B * a.H_q + row) * (2 + D)));
+                for (int k = 0; k < count; ++k)
+                    M = fmaxf(M, __ldcg(a.parts + ((size_t)((c_first + k) * 2 + (k == 0)) * 8 + h) * (2 + D)));
                 float L = 0.0f, O = 0.0f;
                 if (M != -INFINITY) {
-                    for (int sp = 0; sp < a.n_split; ++sp) {
-                        const float* pr = a.parts + ((size_t)sp * g.B * a.H_q + row) * (2 + D);
+                    for (int k = 0; k < count; ++k) {
+                        const float* pr = a.parts + ((size_t)((c_first + k) * 2 + (k == 0)) * 8 + h) * (2 + D);
                         const float l = __ldcg(pr + 1);
                         if (l == 0.0f) continue;
-                        const float wgt = l * exp2f(__ldcg(pr) - M);
+                        const float wgt = l * fexp2(__ldcg(pr) - M);
                         L += wgt;
                         O += wgt * __ldcg(pr + 2 + c);
                     }
                 }
-                write_row(a.out, a.final_mode, row, c, M, L, O);
+                write_row(a.out, a.out_mode, row, c, M, L, O);
             }
             if (tid == 0) a.counters[bh] = 0;
         }
     }
+}
+
+// ---- Stream-K work split over all (b, kv head) units --------------------------------------------------
+// Unit u = (b, hk) costs unit_cost(S_b) work units: its main tiles plus ceil(tail tokens / 8) (the tail is
+// processed a token at a time, ~4x the per-token cost of a tile), at least 1 so that every unit has an
+// owner.  The flattened space [0, C) of all units is cut into n equal contiguous ranges, one per CTA
+// (n = resident CTAs: one balanced wave instead of ragged waves of whole splits).  A CTA walks the units
+// its range touches; a unit inside one CTA is written directly, a unit cut across CTAs is merged by the
+// last of them (partials: slot 1 in the unit's first CTA, slot 0 in the others).
+// the CTA whose range [c C / n, (c + 1) C / n) holds position x
+__device__ __forceinline__ int cta_of(long long x, long long C, int n) { return (int)(((x + 1) * n - 1) / C); }
+
+template <int KB, int VB, int GM>
+__global__ void __launch_bounds__(kThreads, GM == 4 ? KVT_MINB : 3) decode_mma_kernel(DecodeArgs a) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ long long s_wsum[kWarps];
+    __shared__ long long s_first[2];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int B = a.g.B, H = a.g.H;
+    // (1) exclusive scan of the per-batch costs H * cost(S_b): thread = a chunk of consecutive b
+    const int chunk = (B + kThreads - 1) / kThreads;
+    const int b0 = min(tid * chunk, B), b1 = min(b0 + chunk, B);
+    long long mine = 0;
+    for (int bb = b0; bb < b1; ++bb) mine += (long long)H * unit_cost(a.g, a.seq_len[bb]).cost;
+    long long inc = mine;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const long long v = __shfl_up_sync(kFull, inc, off);
+        if (lane >= off) inc += v;
+    }
+    if (lane == 31) s_wsum[warp] = inc;
+    __syncthreads();
+    long long C = 0, excl = inc - mine;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+        if (w < warp) excl += s_wsum[w];
+        C += s_wsum[w];
+    }
+    const int n = (long long)a.n_cta < C ? a.n_cta : (int)C;
+    const int cta = blockIdx.x;
+#if KVT_TRACE
+    unsigned long long t_start;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+#endif
+    if (cta >= n) return;                                   // uniform per CTA
+    const long long lo = (long long)cta * C / n, hi = (long long)(cta + 1) * C / n;
+    if (lo >= excl && lo < excl + mine) {
+        long long P = excl;
+        for (int bb = b0; bb < b1; ++bb) {
+            const long long cb = (long long)H * unit_cost(a.g, a.seq_len[bb]).cost;
+            if (lo < P + cb) { s_first[0] = bb; s_first[1] = P; break; }
+            P += cb;
+        }
+    }
+    __syncthreads();
+    int b = (int)s_first[0];
+    long long Pb = s_first[1], pos = lo;
+    while (pos < hi) {
+        const UnitCost uc = unit_cost(a.g, a.seq_len[b]);
+        if (pos >= Pb + (long long)H * uc.cost) { Pb += (long long)H * uc.cost; ++b; continue; }
+        const int hk = (int)((pos - Pb) / uc.cost);
+        const long long Pu = Pb + (long long)hk * uc.cost;
+        const int x0 = (int)(pos - Pu);
+        const int x1 = (int)(hi - Pu < uc.cost ? hi - Pu : uc.cost);
+        const int cf = cta_of(Pu, C, n), cl = cta_of(Pu + uc.cost - 1, C, n);
+        segment<KB, VB, GM>(a, smem, b, hk, min(x0, uc.tiles), min(x1, uc.tiles), x1 == uc.cost, cta,
+                            cta == cf ? 1 : 0, cf, cl - cf + 1);
+        pos = Pu + x1;
+        __syncthreads();                                    // the next segment reuses shared memory
+    }
+#if KVT_TRACE
+    if (tid == 0) {
+        unsigned long long t_end;
+        unsigned smid;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        if (a.trace && cta < 4096) { a.trace[3 * cta] = smid; a.trace[3 * cta + 1] = t_start; a.trace[3 * cta + 2] = t_end; }
+    }
+#endif
 }
 
 }  // namespace mma

@@ -166,6 +166,31 @@ def test_decode_without_host_lengths(kvt, oracle):
     assert (a - b).abs().max().item() <= 5e-4 * a.abs().max().item()
 
 
+def test_decode_plan_far_above_lengths(kvt, oracle):
+    """Planning from a capacity far above the actual lengths (host lengths absent): the tensor-core kernel's
+    stream-K grid is sized for the capacity and clamps to the actual total work on the device."""
+    spec = kvt.LayerSpec.kivi(2, 2)
+    lens = [3, 40, 0, 65]
+    B, H, g = len(lens), 2, 4
+    K = kvt_synth.keys((B, H, 65, D), seed=11).cuda()
+    V = kvt_synth.values((B, H, 65, D), seed=12).cuda()
+    q = kvt_synth.queries((B, H * g, D), seed=13).cuda()
+    cache = _prefill(kvt, spec, K, V, lens, 65536)
+    sl = torch.tensor(lens, dtype=torch.int32, device="cuda")
+    out = kvt.decode_attention(cache, q, sl, seq_len_host=None, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    Kb, Vb, qb = kvt_synth.bf16_bits(K), kvt_synth.bf16_bits(V), kvt_synth.bf16_bits(q)
+    o = out.cpu().numpy()
+    for b, S in enumerate(lens):
+        for h in range(H):
+            rows = slice(h * g, (h + 1) * g)
+            if S == 0:
+                assert np.all(o[b, rows] == 0)
+                continue
+            ref = oracle.decode_reference(1, 2, 2, 32, 32, D, Kb[b, h, :S], Vb[b, h, :S], qb[b, rows], 1 / math.sqrt(D))
+            assert rel_row_err(o[b, rows], ref).max() <= TOL
+
+
 @pytest.mark.parametrize("n_shards", [2, 4])
 def test_sequence_shards_combine(kvt, oracle, n_shards):
     """a6: shard r holds tokens [r S/N, (r+1) S/N) (non-final shards fully quantised: residual 0);
@@ -191,7 +216,8 @@ def test_sequence_shards_combine(kvt, oracle, n_shards):
         for h in range(H):
             ref = oracle.decode_reference(1, 4, 2, 32, 32, D, Kb[b, h], Vb[b, h], qb[b, h * g:(h + 1) * g], 1 / math.sqrt(D))
             assert rel_row_err(out[b, h * g:(h + 1) * g].cpu().numpy(), ref).max() <= TOL
-    assert (out - ref_gpu).abs().max().item() <= 1e-5 * ref_gpu.abs().max().item()
+    # a different work partition changes only the rounding of the fp16 PV weights (A23)
+    assert (out - ref_gpu).abs().max().item() <= 5e-4 * ref_gpu.abs().max().item()
 
 
 @pytest.mark.parametrize("mode,R", [(0, 0), (1, 32)])

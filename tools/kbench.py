@@ -41,7 +41,7 @@ for i in range(a.reps + 3):
     flush.zero_()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
-    kvt.decode_attention(cache, q, sl, scale=1 / math.sqrt(128), out=out, workspace=ws)
+    kvt.decode_attention(cache, q, sl, seq_len_host=[a.S] * a.B, scale=1 / math.sqrt(128), out=out, workspace=ws)
     e.record()
     torch.cuda.synchronize()
     if i >= 3:

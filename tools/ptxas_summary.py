@@ -1,5 +1,5 @@
 import re, sys
-log = open('paper_2502_04420_b200/build/ptxas.log').read()
+log = open('paper_2502_04420_b200/build/' + (__import__('sys').argv[1] if len(__import__('sys').argv)>1 else 'base') + '/ptxas.log').read()
 cur = None; spill = ''
 for line in log.splitlines():
     m = re.search(r"Compiling entry function '(\S+)'", line)

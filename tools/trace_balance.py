@@ -1,0 +1,61 @@
+"""Load-balance study of the tensor-core decode kernel (needs a KVT_TRACE=1 build):
+    KVT_LIB=libkvt_trace.so python tools/trace_balance.py --kb 4 --vb 2 [--B 64 --S 8192]
+Prints the kernel span, per-CTA durations and per-SM busy time from %globaltimer stamps."""
+import argparse
+import ctypes
+import math
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+import paper_2502_04420_b200 as kvt
+from paper_2502_04420_b200 import kvt as kmod
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--kb", type=int, default=4)
+ap.add_argument("--vb", type=int, default=2)
+ap.add_argument("--B", type=int, default=64)
+ap.add_argument("--H", type=int, default=8)
+ap.add_argument("--g", type=int, default=4)
+ap.add_argument("--S", type=int, default=8192)
+a = ap.parse_args()
+dev = torch.device("cuda")
+spec = kvt.LayerSpec.kivi(a.kb, a.vb)
+cache = kvt.LayerCache(spec, a.B, a.H, 128, a.S)
+gen = torch.Generator(device=dev).manual_seed(1)
+K = torch.randn(a.B, a.H, a.S, 128, device=dev, generator=gen).bfloat16()
+V = torch.randn(a.B, a.H, a.S, 128, device=dev, generator=gen).bfloat16()
+kvt.quantize_append(cache, K, V, torch.zeros(a.B, dtype=torch.int32, device=dev),
+                    torch.full((a.B,), a.S, dtype=torch.int32, device=dev), n_new_max=a.S)
+del K, V
+q = (0.5 * torch.randn(a.B, a.H * a.g, 128, device=dev, generator=gen)).bfloat16()
+sl = torch.full((a.B,), a.S, dtype=torch.int32, device=dev)
+ws = torch.zeros(max(kvt.decode_workspace_bytes(cache, a.H * a.g, [a.S] * a.B), 16), dtype=torch.uint8, device=dev)
+flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+for _ in range(5):
+    flush.zero_()
+    kvt.decode_attention(cache, q, sl, scale=1 / math.sqrt(128), workspace=ws)
+torch.cuda.synchronize()
+buf = (ctypes.c_ulonglong * (3 * 4096))()
+assert kmod._lib.kvt_debug_trace(buf, 4096) == 0
+t = np.frombuffer(buf, dtype=np.uint64).reshape(4096, 3).astype(np.int64)
+t = t[t[:, 2] > 0]
+sm, st, en = t[:, 0], t[:, 1] - t[:, 1].min(), t[:, 2] - t[:, 1].min()
+dur = en - st
+print(f"CTAs {len(t)}  span {en.max() / 1e3:.1f} us   start spread {st.max() / 1e3:.1f} us")
+print(f"CTA duration us: min {dur.min() / 1e3:.1f}  p10 {np.percentile(dur, 10) / 1e3:.1f}  median {np.median(dur) / 1e3:.1f}"
+      f"  p90 {np.percentile(dur, 90) / 1e3:.1f}  max {dur.max() / 1e3:.1f}")
+print(f"CTA end us: min {en.min() / 1e3:.1f}  p10 {np.percentile(en, 10) / 1e3:.1f}  median {np.median(en) / 1e3:.1f}  max {en.max() / 1e3:.1f}")
+per = {}
+for s_, e_ in zip(sm, en):
+    per.setdefault(int(s_), []).append(e_)
+cnt = np.array([len(v) for v in per.values()])
+last = np.array([max(v) for v in per.values()])
+print(f"SMs used {len(per)}  CTAs/SM min {cnt.min()} max {cnt.max()}  SM last-end us: min {last.min() / 1e3:.1f} median {np.median(last) / 1e3:.1f} max {last.max() / 1e3:.1f}")
+order = np.argsort(np.array(list(per.keys())))
+keys = np.array(list(per.keys()))[order]
+print("SM last-end (us) by SM id:", " ".join(f"{int(k)}:{last[i] / 1e3:.0f}" for i, k in zip(order, keys)))
