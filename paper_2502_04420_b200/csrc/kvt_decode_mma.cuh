@@ -296,7 +296,9 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
     float* tail_s = reinterpret_cast<float*>(smem + Gm::Q_BYTES);          // [GM][2 + D]
     uint8_t* body = smem + Gm::Q_BYTES + Gm::TAIL_BYTES;
     const Geometry& g = a.g;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // warp index through a lane-0 shuffle: the compiler then knows it is warp-uniform, so the per-warp TMA
+    // addresses live in uniform registers (no per-copy R2UR broadcast loop around UBLKCP)
+    const int tid = threadIdx.x, lane = tid & 31, warp = __shfl_sync(kFull, tid >> 5, 0);
     const int gid = lane >> 2, tig = lane & 3;
     const int gq = a.gq;
     const int S = a.seq_len[b];
@@ -552,8 +554,7 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
 #else
             // the largest scale: positive bf16 bit patterns order like their values
             uint32_t smb = max(max(mw[0] & 0xffffu, mw[1] & 0xffffu), max(mw[2] & 0xffffu, mw[3] & 0xffffu));
-#pragma unroll
-            for (int off = 16; off >= 1; off >>= 1) smb = max(smb, __shfl_xor_sync(kFull, smb, off));
+            smb = __reduce_max_sync(kFull, smb);                 // REDUX: one instruction for the warp max
             const int sbx = 7 - frexp_e(bf2f(smb));
 #endif
             const float ssc = pow2(sbx);
@@ -726,10 +727,9 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
 #pragma unroll
                     for (int gr = 0; gr < NGL; ++gr) smb = max(smb, mw[mt][r][gr] & 0xffffu);
                 }
-            if constexpr (GM == 4) smb = max(smb, __shfl_xor_sync(kFull, smb, 2));
-            smb = max(smb, __shfl_xor_sync(kFull, smb, 4));
-            smb = max(smb, __shfl_xor_sync(kFull, smb, 8));
-            smb = max(smb, __shfl_xor_sync(kFull, smb, 16));
+            // lanes differing only in tig hold the same tokens (and, GM == 4, the same groups up to the tig^2
+            // split), so the max over the whole warp is the max over all 32 tokens and 4 groups
+            smb = __reduce_max_sync(kFull, smb);
             const int kt = 7 - frexp_e(bf2f(smb));
             if (kt < kp) {
                 if (it > 0) { kfac = pow2(kt - kp); resc = true; }
