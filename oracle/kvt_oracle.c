@@ -165,15 +165,18 @@ int kvto_slice_bytes(int mode, int kb, int vb, int G, int R, int d, int cap, siz
 static size_t vblk_byte(int bits, int tau, int gam, int i, int k) {
     int ks = tau / 16, r = tau % 16;
     if (bits == 2) {            /* one byte; word = [tok j, tok j+4, tok j+8, tok j+12], j = r mod 4 */
-        size_t w = ((size_t)((ks * 4 + r % 4) * 8 + i) * 4 + gam);
+        size_t w = ((size_t)((ks * 8 + i) * 4 + r % 4) * 4 + gam);
         return 4 * w + 2 * (size_t)(r / 8) + (size_t)((r % 8) / 4);
     }
     if (bits == 4) {            /* two bytes; word = [tok j (16 bits) | tok j+8 (16 bits)], j = r mod 8 */
-        size_t w = ((size_t)((ks * 8 + r % 8) * 8 + i) * 4 + gam);
+        int j = r % 8;
+        size_t w = ((size_t)(((ks * 2 + j / 4) * 8 + i) * 4 + j % 4) * 4 + gam);
         return 4 * w + 2 * (size_t)(r / 8) + (size_t)k;
     }
     /* bits == 8: four bytes (channels e = k); words [tok.c0, tok+8.c0, tok.c1, tok+8.c1], [.c2, .., .c3] */
-    size_t w = ((size_t)((ks * 8 + r % 8) * 8 + i) * 4 + gam) * 2 + (size_t)(k / 2);
+    int j = r % 8;
+    size_t u = (size_t)((((ks * 2 + j / 4) * 2 + gam / 2) * 8 + i) * 4 + j % 4);
+    size_t w = u * 4 + (size_t)(gam % 2) * 2 + (size_t)(k / 2);
     return 4 * w + 2 * (size_t)(k % 2) + (size_t)(r / 8);
 }
 

@@ -172,21 +172,22 @@ struct VRaw {                                  // the raw blocked words of one k
 
 template <int VB>
 __device__ __forceinline__ void v_load(const uint8_t* vblk, int ks, int tig, int gid, VRaw<VB>& r) {
+    // uint4 index ((ks*2 + j/4)*8 + gid)*4 + j%4 (token pair j): the 8 lanes of each LDS.128 phase read 128
+    // consecutive bytes, so the loads are free of bank conflicts
     const uint4* w4 = reinterpret_cast<const uint4*>(vblk);
     if constexpr (VB == 4) {
-        // word ((ks*8 + j)*8 + gid)*4 + γ = [tok 16ks+j (16 bits) | tok 16ks+j+8 (16 bits)], j = tig, tig+4
-        const uint4 a = w4[(ks * 8 + tig) * 8 + gid], b = w4[(ks * 8 + tig + 4) * 8 + gid];
+        // word = [tok 16ks+j (16 bits) | tok 16ks+j+8 (16 bits)] of the 4 groups, j = tig (a) and tig + 4 (b)
+        const uint4 a = w4[((ks * 2) * 8 + gid) * 4 + tig], b = w4[((ks * 2 + 1) * 8 + gid) * 4 + tig];
         r.a[0] = a.x; r.a[1] = a.y; r.a[2] = a.z; r.a[3] = a.w;
         r.b[0] = b.x; r.b[1] = b.y; r.b[2] = b.z; r.b[3] = b.w;
     } else if constexpr (VB == 2) {
-        // word ((ks*4 + j)*8 + gid)*4 + γ = bytes [tok j, tok j+4, tok j+8, tok j+12] (+16ks), j = tig
-        const uint4 a = w4[(ks * 4 + tig) * 8 + gid];
+        // word ((ks*8 + gid)*4 + j)*4 + γ = bytes [tok j, tok j+4, tok j+8, tok j+12] (+16ks), j = tig
+        const uint4 a = w4[(ks * 8 + gid) * 4 + tig];
         r.a[0] = a.x; r.a[1] = a.y; r.a[2] = a.z; r.a[3] = a.w;
     } else {
-        // words (((ks*8 + j)*8 + gid)*4 + γ)*2 + {0,1} = [T.c0, T8.c0, T.c1, T8.c1], [T.c2, T8.c2, T.c3, T8.c3]
-        const uint4* pa = w4 + ((ks * 8 + tig) * 8 + gid) * 2;
-        const uint4* pb = w4 + ((ks * 8 + tig + 4) * 8 + gid) * 2;
-        const uint4 a0 = pa[0], a1 = pa[1], b0 = pb[0], b1 = pb[1];
+        // uint4 (((ks*2 + j/4)*2 + γ/2)*8 + gid)*4 + j%4 = words [γ][c pair] = [T.c0, T8.c0, T.c1, T8.c1], [T.c2, ..]
+        const uint4 a0 = w4[(((ks * 2) * 2) * 8 + gid) * 4 + tig], a1 = w4[(((ks * 2) * 2 + 1) * 8 + gid) * 4 + tig];
+        const uint4 b0 = w4[(((ks * 2 + 1) * 2) * 8 + gid) * 4 + tig], b1 = w4[(((ks * 2 + 1) * 2 + 1) * 8 + gid) * 4 + tig];
         r.a[0] = a0.x; r.a[1] = a0.y; r.a[2] = a0.z; r.a[3] = a0.w; r.a[4] = a1.x; r.a[5] = a1.y; r.a[6] = a1.z; r.a[7] = a1.w;
         r.b[0] = b0.x; r.b[1] = b0.y; r.b[2] = b0.z; r.b[3] = b0.w; r.b[4] = b1.x; r.b[5] = b1.y; r.b[6] = b1.z; r.b[7] = b1.w;
     }
@@ -240,9 +241,12 @@ struct Geo {
     static constexpr int NS = KVT_NS;                    // cp.async ring depth per warp
     // per warp: ring + PV weight tile (half2 [4 γ][2 ks][8 pairs][8 heads]) + key scale slots (half2 [4][16])
     static constexpr int W_OFF = NS * STAGE;
-    static constexpr int W_BYTES = 4 * 2 * 8 * 8 * 4;
+    // half2 [4 γ][2 ks][8 pairs][8 heads], γ >= 2 shifted by 4 words (the tig / tig^2 lanes that store
+    // γ and γ + 2 in one STS.64 then hit different banks)
+    static constexpr int W_BYTES = 4 * 2 * 8 * 8 * 4 + 16;
     static constexpr int SH_OFF = W_OFF + W_BYTES;
-    static constexpr int BAR_OFF = SH_OFF + 4 * 16 * 4;           // one mbarrier per stage
+    static constexpr int SH_STRIDE = 20;                          // words per tig row (16 used; padding: no bank conflicts)
+    static constexpr int BAR_OFF = SH_OFF + 4 * SH_STRIDE * 4;    // one mbarrier per stage
     static constexpr int WARP_BYTES = BAR_OFF + 8 * NS;
     static constexpr int Q_BYTES = GM * D * 4;           // q fp32 [GM][128]
     static constexpr int TAIL_PART = ((GM * (2 + D) * 4) + 15) / 16 * 16;    // tail partial (m, l, o) [GM]
@@ -305,7 +309,7 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
 
     uint8_t* wbase = body + warp * Gm::WARP_BYTES;
     uint32_t* w_s = reinterpret_cast<uint32_t*>(wbase + Gm::W_OFF);        // half2 [4][2][8][8]
-    uint32_t* sh_s = reinterpret_cast<uint32_t*>(wbase + Gm::SH_OFF);      // half2 [4 tig][16 slots]
+    uint32_t* sh_s = reinterpret_cast<uint32_t*>(wbase + Gm::SH_OFF);      // half2 [4 tig][SH_STRIDE]
 
     {   // q -> shared fp32 (zero for padded heads)
         const uint16_t* qg = a.q + ((size_t)b * a.H_q + (size_t)hk * gq) * D;
@@ -565,7 +569,7 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
             for (int e = 0; e < 4; ++e) {
                 const int c = 4 * lane + e;
                 const int code = k_slot_of<KB>(c & 31);
-                shh[((c >> 5) * 16 + (code >> 1)) * 2 + (code & 1)] = __float2half_rn(bf2f(mw[e] & 0xffffu) * ssc);
+                shh[((c >> 5) * Gm::SH_STRIDE + (code >> 1)) * 2 + (code & 1)] = __float2half_rn(bf2f(mw[e] & 0xffffu) * ssc);
                 z[e] = bf2f(mw[e] >> 16);
             }
             // bias partials of the GM heads, reduce-scattered: lane l ends with head (l & 7)
@@ -610,7 +614,7 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
         // (2) B operand of QK: q_h * s_h split exactly into hi + lo
         uint32_t bq[16], bq_lo[(GM == 8) ? 16 : 1];
         {
-            const uint4* shv = reinterpret_cast<const uint4*>(sh_s + tig * 16);
+            const uint4* shv = reinterpret_cast<const uint4*>(sh_s + tig * Gm::SH_STRIDE);
             // GM == 4: lanes gid >= 4 carry the lo halves: b = fma(q, s, -f * hi) with f = 1 (lo) or 0 (hi)
             const __half2 negf = __float2half2_rn((GM == 4 && gid >= 4) ? -1.0f : 0.0f);
 #pragma unroll
@@ -755,7 +759,7 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
                     const float2 wa = dec::fmul2(pk[mt][0], sv), wb = dec::fmul2(pk[mt][1], sv);
                     wv.x = h2u(__floats2half2_rn(wa.x, wa.y));
                     wv.y = h2u(__floats2half2_rn(wb.x, wb.y));
-                    *reinterpret_cast<uint2*>(w_s + ((gam * 2 + mt) * 8 + gid) * 8 + hA) = wv;
+                    *reinterpret_cast<uint2*>(w_s + ((gam * 2 + mt) * 8 + gid) * 8 + 4 * (gam >> 1) + hA) = wv;
                     const float z0 = __uint_as_float(w0 & 0xffff0000u), z1 = __uint_as_float(w1 & 0xffff0000u);
                     za = dec::ffma2(make_float2(p[mt][0][0], p[mt][0][1]), make_float2(z0, z0), za);
                     za = dec::ffma2(make_float2(p[mt][1][0], p[mt][1][1]), make_float2(z1, z1), za);
@@ -778,7 +782,7 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
                 v_load<VB>(vc_s, ks, tig, gid, raw);
 #pragma unroll
                 for (int gam = 0; gam < 4; ++gam) {
-                    const uint32_t* wr = w_s + (gam * 2 + ks) * 64 + gid;
+                    const uint32_t* wr = w_s + (gam * 2 + ks) * 64 + 4 * (gam >> 1) + gid;
                     const uint32_t b0 = wr[tig * 8], b1 = wr[(tig + 4) * 8];
                     uint32_t hA4[4], hB4[4];
                     v_frag<VB>(raw, gam, hA4, hB4);

@@ -34,16 +34,17 @@ __host__ __device__ inline int row_bytes(int d, int bits) { return bits == 16 ? 
 // (gam, i) = channels 32 gam + 4 i .. + 3 of the token at position tau of the block.  Tokens tau and
 // tau + 8 of each 16-token half share 32-bit words, so the PV operand pairs load directly.
 __host__ __device__ inline uint32_t vblk_off(int bits, int tau, int gam, int i, int k) {
-    const int ks = tau >> 4, r = tau & 15;
+    const int ks = tau >> 4, r = tau & 15, j = r & 7;
     if (bits == 2) {
-        const uint32_t w = (uint32_t)(((ks * 4 + (r & 3)) * 8 + i) * 4 + gam);
+        const uint32_t w = (uint32_t)(((ks * 8 + i) * 4 + (r & 3)) * 4 + gam);
         return 4 * w + 2 * (uint32_t)(r >> 3) + (uint32_t)((r & 7) >> 2);
     }
     if (bits == 4) {
-        const uint32_t w = (uint32_t)(((ks * 8 + (r & 7)) * 8 + i) * 4 + gam);
+        const uint32_t w = (uint32_t)((((ks * 2 + (j >> 2)) * 8 + i) * 4 + (j & 3)) * 4 + gam);
         return 4 * w + 2 * (uint32_t)(r >> 3) + (uint32_t)k;
     }
-    const uint32_t w = (uint32_t)((((ks * 8 + (r & 7)) * 8 + i) * 4 + gam) * 2 + (k >> 1));
+    const uint32_t u = (uint32_t)((((ks * 2 + (j >> 2)) * 2 + (gam >> 1)) * 8 + i) * 4 + (j & 3));
+    const uint32_t w = u * 4 + (uint32_t)(gam & 1) * 2 + (uint32_t)(k >> 1);
     return 4 * w + 2 * (uint32_t)(k & 1) + (uint32_t)(r >> 3);
 }
 

@@ -14,5 +14,6 @@ for w in "$@"; do
 done
 if [ "$NCU" == "1" ]; then
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"decode|combine|append" -s 100 -c 200 --csv --log-file gpurun_out/launches.csv python bench.py --profile --steps 3 --warmup 2 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:decode_ -s 40 -c 2 -o gpurun_out/prof_decode -f python bench.py --profile --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
+# the dominant kernel (K4V2 layers, 20 of 32 in llama-3.25) at the bench launch configuration (B=64, S=8192)
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:decode_mma -s 2 -c 1 -o gpurun_out/prof_decode -f python tools/kbench.py --kb 4 --vb 2 --reps 1 > gpurun_out/ncu_full.log 2>&1
 fi
