@@ -82,6 +82,19 @@ __device__ __forceinline__ Mul make_mul() {
 #ifndef KVT_TRACE
 #define KVT_TRACE 0    // debug builds only: per-CTA (SM, start, end) timestamps for load-balance studies
 #endif
+#if KVT_TRACE
+#define KVT_STAMP(k)                                                                                     \
+    do {                                                                                                 \
+        if (a.trace && tid == 0 && blockIdx.x < 4096) {                                                  \
+            unsigned long long t_;                                                                       \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                       \
+            unsigned long long* p_ = a.trace + 3 * 4096 + 8 * blockIdx.x + (k);                          \
+            if (*p_ == 0ull) *p_ = t_;                                                                   \
+        }                                                                                                \
+    } while (0)
+#else
+#define KVT_STAMP(k) do { } while (0)
+#endif
 #ifndef KVT_EXP
 #define KVT_EXP 0      // profiling experiments only: 1 = skip PV, 2 = skip QK
 #endif
@@ -306,6 +319,7 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
     const int gid = lane >> 2, tig = lane & 3;
     const int gq = a.gq;
     const int S = a.seq_len[b];
+    KVT_STAMP(0);
 
     uint8_t* wbase = body + warp * Gm::WARP_BYTES;
     uint32_t* w_s = reinterpret_cast<uint32_t*>(wbase + Gm::W_OFF);        // half2 [4][2][8][8]
@@ -405,6 +419,7 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
     // GM == 4: lanes tig and tig^2 hold the same probabilities, so they prepare different value groups:
     // relative group r (0, 1) of this lane is group 2 * (tig >> 1) + r.
     const int gsh = (GM == 4) ? 2 * (tig >> 1) : 0;
+    KVT_STAMP(4);
     const Mul kmul = make_mul();
     constexpr int NGL = (GM == 4) ? 2 : 4;               // value groups prepared per lane
 
@@ -432,6 +447,7 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
             ot[h][0] = ot[h][1] = ot[h][2] = ot[h][3] = 0.0f;
         }
         if (staged) mbar_wait(tbar, 0);
+        KVT_STAMP(5);
         if (KVT_EXP != 5 && do_tail) {
             // KVT_TAILN tokens per iteration: all loads first, then four independent dot/shuffle chains
             for (int t0 = n_main + warp; t0 < S; t0 += KVT_TAILN * kWarps) {
@@ -487,6 +503,7 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
         }
     }
     __syncthreads();
+    KVT_STAMP(6);
     {   // merge the warps' tail partials: thread = channel
         const int c = tid;
         const float* sc = reinterpret_cast<const float*>(body);
@@ -511,6 +528,7 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
     }
     if (staged && tid == 0) asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(tbar)));
     __syncthreads();
+    KVT_STAMP(7);
     // ---- per-warp TMA ring: lane 0 issues four bulk copies per tile onto the stage's mbarrier ----
     uint64_t* bars = reinterpret_cast<uint64_t*>(wbase + Gm::BAR_OFF);
     if (lane == 0) {
@@ -534,6 +552,7 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
 #pragma unroll
     for (int s = 0; s < Gm::NS - 1; ++s)
         if (s < n_my) issue(s, s);
+    KVT_STAMP(1);
     for (int it = 0; it < n_my; ++it) {
         {
             const int nx = it + Gm::NS - 1;
@@ -794,6 +813,7 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
         __syncwarp();
     }
 
+    KVT_STAMP(2);
     __syncwarp();
     if (lane == 0) {
 #pragma unroll
@@ -905,6 +925,7 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
             if (tid == 0) a.counters[bh] = 0;
         }
     }
+    KVT_STAMP(3);
 }
 
 // ---- Stream-K work split over all (b, kv head) units --------------------------------------------------

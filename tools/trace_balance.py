@@ -40,10 +40,22 @@ for _ in range(5):
     flush.zero_()
     kvt.decode_attention(cache, q, sl, scale=1 / math.sqrt(128), workspace=ws)
 torch.cuda.synchronize()
-buf = (ctypes.c_ulonglong * (3 * 4096))()
+buf = (ctypes.c_ulonglong * (11 * 4096))()
 assert kmod._lib.kvt_debug_trace(buf, 4096) == 0
-t = np.frombuffer(buf, dtype=np.uint64).reshape(4096, 3).astype(np.int64)
-t = t[t[:, 2] > 0]
+allb = np.frombuffer(buf, dtype=np.uint64).astype(np.int64)
+t = allb[:3 * 4096].reshape(4096, 3)
+st4 = allb[3 * 4096:].reshape(4096, 8)
+keep = t[:, 2] > 0
+t, st4 = t[keep], st4[keep]
+t0 = t[:, 1].min()
+if (st4[:, 0] > 0).all():
+    ph = lambda a_, b_: (st4[:, b_] - st4[:, a_]) / 1e3
+    q = lambda x: f"min {x.min():.1f} med {np.median(x):.1f} max {x.max():.1f}"
+    print("first segment phases (us): launch->seg start", q((st4[:, 0] - t0) / 1e3), "| prologue", q(ph(0, 1)),
+          "| main loop (warp 0)", q(ph(1, 2)), "| epilogue", q(ph(2, 3)))
+    if (st4[:, 7] > 0).all():
+        print("  prologue split (us): q setup", q(ph(0, 4)), "| tail wait", q(ph(4, 5)), "| tail compute", q(ph(5, 6)),
+              "| tail merge", q(ph(6, 7)), "| ring start", q(ph(7, 1)))
 sm, st, en = t[:, 0], t[:, 1] - t[:, 1].min(), t[:, 2] - t[:, 1].min()
 dur = en - st
 print(f"CTAs {len(t)}  span {en.max() / 1e3:.1f} us   start spread {st.max() / 1e3:.1f} us")
