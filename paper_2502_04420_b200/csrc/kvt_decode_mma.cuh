@@ -76,9 +76,6 @@ __device__ __forceinline__ Mul make_mul() {
 #ifndef KVT_FIXK
 #define KVT_FIXK 0     // 1: no per-block key-scale exponent (q scaled to <= 2^3 instead)
 #endif
-#ifndef KVT_TAILN
-#define KVT_TAILN 4    // tail tokens per warp iteration (loads batched ahead of the math)
-#endif
 #ifndef KVT_TRACE
 #define KVT_TRACE 0    // debug builds only: per-CTA (SM, start, end) timestamps for load-balance studies
 #endif
@@ -434,96 +431,125 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
     for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.0f;
     int kp = 126;                  // PV weight exponent (only decreases)
 
-    // ---- tail tokens [n_main, S) first: token at a time, lane = channels [4 lane, 4 lane + 4).  Run before
-    // the main loop (its dependent global loads would otherwise sit at the end of the CTA, when the whole
-    // wave ends together and memory latency is at its worst); per-warp partials go to scratch in the ring
-    // area, which the TMA ring only uses afterwards, and are merged into tail_s. ----
+    // ---- tail tokens [n_main, S) first (before the main loop: at the end of the CTA the whole wave finishes
+    // together and these dependent loads would sit on the critical path).  Super-chunks of <= 128 tokens:
+    //   (1) QK: lane = token, warp = a quarter of the channels (4-channel groups rotated by lane, so the
+    //       shared-memory reads of a warp spread over the banks) -> partial logits part[warp][token][head];
+    //   (2) warp h = head h (and h + 4): logits, running max / sum, p[token][head];
+    //   (3) PV: lane = 4 channels, warp = every 4th token -> o partials in registers (rescaled per
+    //       super-chunk); finally summed over the warps into tail_s = (m, l, o) per head. ----
     {
-        float* cw = reinterpret_cast<float*>(body) + warp * GM * (2 + D);
-        float mt_[GM], lt[GM], ot[GM][4];
+        float* part = reinterpret_cast<float*>(body);                      // [kWarps][128][GM] / p [128][GM]
+        float ot[GM][4];
 #pragma unroll
-        for (int h = 0; h < GM; ++h) {
-            mt_[h] = -INFINITY; lt[h] = 0.0f;
-            ot[h][0] = ot[h][1] = ot[h][2] = ot[h][3] = 0.0f;
-        }
+        for (int h = 0; h < GM; ++h) ot[h][0] = ot[h][1] = ot[h][2] = ot[h][3] = 0.0f;
+        if (tid < GM) { tail_s[tid * (2 + D)] = -INFINITY; tail_s[tid * (2 + D) + 1] = 0.0f; }
         if (staged) mbar_wait(tbar, 0);
         KVT_STAMP(5);
-        if (KVT_EXP != 5 && do_tail) {
-            // KVT_TAILN tokens per iteration: all loads first, then four independent dot/shuffle chains
-            for (int t0 = n_main + warp; t0 < S; t0 += KVT_TAILN * kWarps) {
-                float kx[KVT_TAILN][4], vx[KVT_TAILN][4];
+        const int T = (KVT_EXP != 5 && do_tail) ? S - n_main : 0;
+        for (int sc0 = 0; sc0 < T; sc0 += 128) {
+            const int Tc = T - sc0 < 128 ? T - sc0 : 128;
+            __syncthreads();                                                 // part / tail_s reuse
+            // (1) partial logits over this warp's 32 channels
+            for (int c0 = 0; c0 < Tc; c0 += 32) {
+                const int i = c0 + lane, t = n_main + sc0 + i;
+                float acc[GM];
 #pragma unroll
-                for (int u = 0; u < KVT_TAILN; ++u) {
-                    const int t = t0 + u * kWarps;
-                    if (t < S) {
-                        dec::tail_k<KB, true>(tl, g, t, nqK, lane, kx[u]);
-                        dec::tail_v<VB, true>(tl, g, t, nqV, lane, vx[u]);
-                    } else {
+                for (int h = 0; h < GM; ++h) acc[h] = 0.0f;
+                if (i < Tc) {
+#pragma unroll 2
+                    for (int jj = 0; jj < 8; ++jj) {
+                        const int c4 = 8 * warp + ((jj + lane) & 7);             // 4-channel group index
+                        float kx[4];
+                        dec::tail_k<KB, true>(tl, g, t, nqK, c4, kx);
 #pragma unroll
-                        for (int i = 0; i < 4; ++i) kx[u][i] = vx[u][i] = 0.0f;
+                        for (int h = 0; h < GM; ++h) {
+                            const float4 qv = *reinterpret_cast<const float4*>(q_s + h * D + 4 * c4);
+                            acc[h] = fmaf(qv.x, kx[0], fmaf(qv.y, kx[1], fmaf(qv.z, kx[2], fmaf(qv.w, kx[3], acc[h]))));
+                        }
                     }
                 }
-                float sc[KVT_TAILN][GM];
+                float* pw = part + ((size_t)warp * 128 + i) * GM;
+                if (i < Tc) {
+#pragma unroll
+                    for (int h = 0; h < GM; h += 4)
+                        *reinterpret_cast<float4*>(pw + h) = make_float4(acc[h], acc[h + 1], acc[h + 2], acc[h + 3]);
+                }
+            }
+            __syncthreads();
+            // logits (log2 domain) of token tid, summed over the 4 channel quarters, into part[0]
+            for (int i = tid; i < Tc; i += kThreads) {
 #pragma unroll
                 for (int h = 0; h < GM; ++h) {
-                    const float4 qv = *reinterpret_cast<const float4*>(q_s + h * D + 4 * lane);
+                    float l = 0.0f;
 #pragma unroll
-                    for (int u = 0; u < KVT_TAILN; ++u)
-                        sc[u][h] = qv.x * kx[u][0] + qv.y * kx[u][1] + qv.z * kx[u][2] + qv.w * kx[u][3];
+                    for (int w = 0; w < kWarps; ++w) l += part[((size_t)w * 128 + i) * GM + h];
+                    part[(size_t)i * GM + h] = l * a.scale_log2;
+                }
+            }
+            __syncthreads();
+            // (2) per head: running max / sum, p = 2^(l - m) in place, rescale factor in tail_s[h][2]
+            for (int h = warp; h < GM; h += kWarps) {
+                float mx = -INFINITY;
+                for (int i = lane; i < Tc; i += 32) mx = fmaxf(mx, part[(size_t)i * GM + h]);
+#pragma unroll
+                for (int off = 16; off >= 1; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, off));
+                float* th = tail_s + h * (2 + D);
+                const float m_old = th[0], m_new = fmaxf(m_old, mx);
+                float sum = 0.0f;
+                for (int i = lane; i < Tc; i += 32) {
+                    const float p = fexp2(part[(size_t)i * GM + h] - m_new);
+                    part[(size_t)i * GM + h] = p;
+                    sum += p;
                 }
 #pragma unroll
-                for (int off = 16; off >= 1; off >>= 1)
+                for (int off = 16; off >= 1; off >>= 1) sum += __shfl_xor_sync(kFull, sum, off);
+                __syncwarp();
+                if (lane == 0) {
+                    const float al = fexp2(m_old - m_new);
+                    th[1] = th[1] * al + sum;
+                    th[0] = m_new;
+                    th[2] = al;
+                }
+            }
+            __syncthreads();
+            // (3) PV: lane = channels [4 lane, 4 lane + 4), warp = tokens i = warp (mod 4)
 #pragma unroll
-                    for (int u = 0; u < KVT_TAILN; ++u)
+            for (int h = 0; h < GM; ++h) {
+                const float al = tail_s[h * (2 + D) + 2];
 #pragma unroll
-                        for (int h = 0; h < GM; ++h) sc[u][h] += __shfl_xor_sync(kFull, sc[u][h], off);
+                for (int e = 0; e < 4; ++e) ot[h][e] *= al;
+            }
+            for (int i = warp; i < Tc; i += kWarps) {
+                float vx[4];
+                dec::tail_v<VB, true>(tl, g, n_main + sc0 + i, nqV, lane, vx);
 #pragma unroll
-                for (int u = 0; u < KVT_TAILN; ++u) {
-                    if (t0 + u * kWarps >= S) break;
+                for (int h = 0; h < GM; h += 4) {
+                    const float4 p4 = *reinterpret_cast<const float4*>(part + (size_t)i * GM + h);
+                    const float pp[4] = {p4.x, p4.y, p4.z, p4.w};
 #pragma unroll
-                    for (int h = 0; h < GM; ++h) {
-                        const float sv = sc[u][h] * a.scale_log2;
-                        const float mn = fmaxf(mt_[h], sv);
-                        const float al = fexp2(mt_[h] - mn);
-                        const float pp = fexp2(sv - mn);
-                        lt[h] = lt[h] * al + pp;
+                    for (int hh = 0; hh < 4; ++hh)
 #pragma unroll
-                        for (int i = 0; i < 4; ++i) ot[h][i] = ot[h][i] * al + pp * vx[u][i];
-                        mt_[h] = mn;
-                    }
+                        for (int e = 0; e < 4; ++e) ot[h + hh][e] = fmaf(pp[hh], vx[e], ot[h + hh][e]);
                 }
             }
         }
+        __syncthreads();                                                     // part -> o partials
+        if (T > 0) {
 #pragma unroll
-        for (int h = 0; h < GM; ++h) {
-            float* ch = cw + h * (2 + D);
-            if (lane == 0) { ch[0] = mt_[h]; ch[1] = lt[h]; }
-#pragma unroll
-            for (int i = 0; i < 4; ++i) ch[2 + 4 * lane + i] = ot[h][i];
+            for (int h = 0; h < GM; ++h)
+                *reinterpret_cast<float4*>(part + ((size_t)warp * GM + h) * D + 4 * lane) =
+                    make_float4(ot[h][0], ot[h][1], ot[h][2], ot[h][3]);
         }
-    }
-    __syncthreads();
-    KVT_STAMP(6);
-    {   // merge the warps' tail partials: thread = channel
-        const int c = tid;
-        const float* sc = reinterpret_cast<const float*>(body);
-        for (int h = 0; h < GM; ++h) {
-            float M = -INFINITY, L = 0.0f, O = 0.0f;
+        __syncthreads();
+        KVT_STAMP(6);
+        for (int h = 0; h < GM; ++h) {                                       // thread = channel
+            float O = 0.0f;
+            if (T > 0) {
 #pragma unroll
-            for (int w = 0; w < kWarps; ++w) M = fmaxf(M, sc[(w * GM + h) * (2 + D)]);
-            if (M != -INFINITY) {
-#pragma unroll
-                for (int w = 0; w < kWarps; ++w) {
-                    const float* cw = sc + (w * GM + h) * (2 + D);
-                    if (cw[1] == 0.0f) continue;
-                    const float scl = fexp2(cw[0] - M);
-                    L += cw[1] * scl;
-                    O += cw[2 + c] * scl;
-                }
+                for (int w = 0; w < kWarps; ++w) O += part[((size_t)w * GM + h) * D + tid];
             }
-            float* th = tail_s + h * (2 + D);
-            if (c == 0) { th[0] = M; th[1] = L; }
-            th[2 + c] = O;
+            tail_s[h * (2 + D) + 2 + tid] = O;
         }
     }
     if (staged && tid == 0) asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(tbar)));
@@ -541,7 +567,6 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
         if (lane != 0) return;
         const int t0 = (tile_lo + warp + it * kWarps) * kTile;
         uint8_t* sb = wbase + st * Gm::STAGE;
-        fence_proxy_async();                      // the stage's previous generic-proxy reads come first
         mbar_expect_tx(bars + st, Gm::STAGE);
         bulk_g2s(sb + Gm::K_OFF, sl.kc + (size_t)t0 * Gm::KROW, kTile * Gm::KROW, bars + st);
         bulk_g2s(sb + Gm::KM_OFF, sl.km + (size_t)(t0 / kTile) * D, D * 4, bars + st);
@@ -549,6 +574,9 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
         bulk_g2s(sb + Gm::VM_OFF, sl.vm + (size_t)t0 * 4, kTile * 16, bars + st);
     };
 
+    // generic-proxy writes to the ring area (tail scratch) are ordered before the first bulk copies; later
+    // refills overwrite a stage whose reads fed the previous tile's MMAs, so they need no proxy fence
+    if (lane == 0) fence_proxy_async();
 #pragma unroll
     for (int s = 0; s < Gm::NS - 1; ++s)
         if (s < n_my) issue(s, s);

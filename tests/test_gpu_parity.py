@@ -40,6 +40,7 @@ SPECS = [
     ("kivi_k2v8", lambda k: k.LayerSpec.kivi(2, 8)),
     ("kivi_k8v2", lambda k: k.LayerSpec.kivi(8, 2)),
     ("kivi_k2v4_r64", lambda k: k.LayerSpec.kivi(2, 4, residual=64)),
+    ("kivi_k4v2_r160", lambda k: k.LayerSpec.kivi(4, 2, residual=160)),   # tail > 128: two tail super-chunks
     ("kivi_k8v4_g64", lambda k: k.LayerSpec.kivi(8, 4, group=64, residual=64)),
     ("kivi_k16v4", lambda k: k.LayerSpec.kivi(16, 4)),
     ("kivi_k4v16", lambda k: k.LayerSpec.kivi(4, 16)),
