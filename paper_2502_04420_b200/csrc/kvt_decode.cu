@@ -162,9 +162,13 @@ static int plan_ctas(const Geometry& g, int plan_len, int occ, int sms) {
     if (forced > 0) return forced;                      // experiments only
     const long long units = (long long)g.B * g.H;
     const long long C = units * dec::unit_cost(g, plan_len).cost;
+    const long long slots = (long long)occ * sms;
+    // whole units when they (nearly) fill the wave: no unit is cut, no merge (measured: 512 units of 255
+    // tiles on 592 slots run 2.5% faster uncut than cut into 592 equal shares)
+    if (units <= slots && 4 * units >= 3 * slots) return (int)units;
     long long n = (C + 15) / 16;                        // cut units only into pieces of >= ~16 work units
     if (n < units) n = units;                           // ... but never leave whole units waiting in line
-    if (n > (long long)occ * sms) n = (long long)occ * sms;
+    if (n > slots) n = slots;
     return n < 1 ? 1 : (int)n;
 }
 

@@ -741,14 +741,18 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
             l4[2] = fmaf(dq[1][j], cs, cb);
             l4[3] = fmaf(dq[1][2 + j], cs, cb);
             float mx = fmaxf(fmaxf(l4[0], l4[1]), fmaxf(l4[2], l4[3]));
-            mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 4));
-            mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 8));
-            mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 16));
             alpha[j] = 1.0f;
-            if (mx > m_run[j] + 8.0f) {
-                alpha[j] = fexp2(m_run[j] - mx);
-                m_run[j] = mx;
-                resc = true;
+            // the reference max moves only if some logit exceeds it by > 8: one vote decides whether the
+            // cross-lane max is needed at all (after the first tiles it almost never is)
+            if (__any_sync(kFull, mx > m_run[j] + 8.0f)) {
+                mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 4));
+                mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 8));
+                mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 16));
+                if (mx > m_run[j] + 8.0f) {
+                    alpha[j] = fexp2(m_run[j] - mx);
+                    m_run[j] = mx;
+                    resc = true;
+                }
             }
             const float mr = m_run[j];
             p[0][0][j] = fexp2(l4[0] - mr);
