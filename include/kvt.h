@@ -96,9 +96,11 @@ int32_t     kvt_validate_spec(const kvt_layer_spec* spec, int32_t head_dim);
  *                 word = bf16 scale (low 16 bits) | bf16 zero-point (high 16 bits)   (A3)
  *   k_resid  bf16 per-token: [B][H][R][d] ring (slot t mod R);  KIVI: [B][H][F][d] linear
  *                 (slot t - n_qK), F = R if R > 0 else G      (none when 16, or per-token R = 0)
- *   v_codes, v_meta, v_resid: as the per-token K buffers with value_bits; for KIVI layers with G = 32,
- *                 d = 128 and 2/4/8-bit K and V the codes of each 32-token block use the blocked layout
- *                 of DESIGN.md §4 (same bytes, tokens t and t + 8 interleaved in 32-bit words).
+ *   v_codes, v_meta, v_resid: as the per-token K buffers with value_bits.
+ * KIVI layers with G = 32, d = 128 and 2/4/8-bit K and V use TILE RECORDS instead:
+ *   k_codes  u8  [B][H][cap/32][rec], rec = 32*(16 kb + 16 vb) + 1024: record j = tokens 32j..32j+31 as
+ *                 [K code rows | K block meta (d u32) | V codes in the blocked layout | V meta (32 x 4 u32)];
+ *   k_meta, v_codes, v_meta are empty (size 0, may be NULL); k_resid / v_resid as above.
  * Token t of a length-S sequence is held quantised iff t < n_q (A6, A7):
  *   per-token tensor: n_q = max(0, S - R);  KIVI key: n_q = F * floor(S / F);  16 bits: n_q = S. */
 typedef struct {

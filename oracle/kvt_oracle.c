@@ -153,6 +153,12 @@ int kvto_slice_bytes(int mode, int kb, int vb, int G, int R, int d, int cap, siz
     out[3] = (size_t)cap * row_bytes(d, vb);
     if (vb == 16) { out[4] = 0; out[5] = 0; }
     else { out[4] = (size_t)cap * (d / G) * 4; out[5] = (size_t)R * d * 2; }
+    if (mode == KVTO_MODE_KIVI && kb != 16 && vb != 16 && G == 32 && d == 128) {
+        /* tile records: K codes, K meta, V codes and V meta of each 32-token block are one
+         * contiguous record in k_codes; k_meta, v_codes and v_meta are empty */
+        out[0] = out[0] + out[1] + out[3] + out[4];
+        out[1] = out[3] = out[4] = 0;
+    }
     return 0;
 }
 
@@ -203,6 +209,50 @@ static void vblk_load(int bits, int t, const uint8_t* codes, uint8_t* row) {
         for (int i = 0; i < 8; ++i)
             for (int k = 0; k < cb; ++k)
                 row[(size_t)(32 * gam + 4 * i) * bits / 8 + k] = blk[vblk_byte(bits, t % 32, gam, i, k)];
+}
+
+/* Tile records, used exactly where the blocked value layout is: the k_codes slice is a
+ * sequence of cap/32 records, record j holding block j (tokens 32j .. 32j+31) as
+ *   [K code rows (32 x d kb/8) | K block meta (d x u32) | V codes, blocked (32 x d vb/8) | V meta (32 x 4 u32)].
+ * The oracle builds the four parts as separate arrays (the same arrays the other layouts store) and moves
+ * the bytes that the history defines into (out of) the records. */
+static size_t rec_bytes(int kb, int vb) { return 32 * (size_t)(16 * kb + 16 * vb) + 1024; }
+
+static void records_store(int kb, int vb, int nqK, int nqV, const uint8_t* kc, const uint32_t* km,
+                          const uint8_t* vc, const uint32_t* vm, uint8_t* rec) {
+    size_t RB = rec_bytes(kb, vb), rk = (size_t)16 * kb, rv = (size_t)16 * vb;
+    for (int t = 0; t < nqK; ++t) memcpy(rec + (size_t)(t / 32) * RB + (size_t)(t % 32) * rk, kc + (size_t)t * rk, rk);
+    for (int j = 0; j < nqK / 32; ++j) memcpy(rec + (size_t)j * RB + 32 * rk, km + (size_t)j * 128, 512);
+    for (int t = 0; t < nqV; ++t) {
+        /* the blocked bytes of token t: every chunk byte of token t in block t / 32 */
+        const uint8_t* blk = vc + (size_t)(t / 32) * 32 * rv;
+        uint8_t* dst = rec + (size_t)(t / 32) * RB + 32 * rk + 512;
+        for (int gam = 0; gam < 4; ++gam)
+            for (int i = 0; i < 8; ++i)
+                for (int k = 0; k < vb / 2; ++k) {
+                    size_t o = vblk_byte(vb, t % 32, gam, i, k);
+                    dst[o] = blk[o];
+                }
+        memcpy(rec + (size_t)(t / 32) * RB + 32 * rk + 512 + 32 * rv + (size_t)(t % 32) * 16, vm + (size_t)t * 4, 16);
+    }
+}
+
+static void records_load(int kb, int vb, int nqK, int nqV, const uint8_t* rec, uint8_t* kc, uint32_t* km,
+                         uint8_t* vc, uint32_t* vm) {
+    size_t RB = rec_bytes(kb, vb), rk = (size_t)16 * kb, rv = (size_t)16 * vb;
+    for (int t = 0; t < nqK; ++t) memcpy(kc + (size_t)t * rk, rec + (size_t)(t / 32) * RB + (size_t)(t % 32) * rk, rk);
+    for (int j = 0; j < nqK / 32; ++j) memcpy(km + (size_t)j * 128, rec + (size_t)j * RB + 32 * rk, 512);
+    for (int t = 0; t < nqV; ++t) {
+        const uint8_t* src = rec + (size_t)(t / 32) * RB + 32 * rk + 512;
+        uint8_t* blk = vc + (size_t)(t / 32) * 32 * rv;
+        for (int gam = 0; gam < 4; ++gam)
+            for (int i = 0; i < 8; ++i)
+                for (int k = 0; k < vb / 2; ++k) {
+                    size_t o = vblk_byte(vb, t % 32, gam, i, k);
+                    blk[o] = src[o];
+                }
+        memcpy(vm + (size_t)t * 4, rec + (size_t)(t / 32) * RB + 32 * rk + 512 + 32 * rv + (size_t)(t % 32) * 16, 16);
+    }
 }
 
 /* Per-token tensor (V in both modes, K in per-token mode): token t < n_q is split into d/G channel
@@ -261,11 +311,24 @@ int kvto_build_cache(int mode, int kb, int vb, int G, int R, int d, int cap, int
                      uint8_t* v_codes, uint32_t* v_meta, uint16_t* v_resid) {
     size_t sz[6];
     if (kvto_slice_bytes(mode, kb, vb, G, R, d, cap, sz) != 0 || S < 0 || S > cap) return -1;
+    if (blocked_v(mode, kb, vb, G, d)) {
+        /* tile records: build the four parts separately, then place them */
+        uint8_t* kc = (uint8_t*)malloc((size_t)cap * 16 * kb + 1);
+        uint32_t* km = (uint32_t*)malloc((size_t)(cap / 32) * 512 + 4);
+        uint8_t* vc = (uint8_t*)malloc((size_t)cap * 16 * vb + 1);
+        uint32_t* vm = (uint32_t*)malloc((size_t)cap * 16 + 4);
+        build_per_channel(kb, G, R, d, S, K, kc, km, k_resid);
+        build_per_token(vb, G, R, d, S, V, vc, vm, v_resid, 1);
+        records_store(kb, vb, kvto_n_quantized_key(mode, kb, G, R, S), kvto_n_quantized_value(mode, vb, G, R, S),
+                      kc, km, vc, vm, k_codes);
+        free(kc); free(km); free(vc); free(vm);
+        return 0;
+    }
     if (mode == KVTO_MODE_KIVI && kb != 16)
         build_per_channel(kb, G, R, d, S, K, k_codes, k_meta, k_resid);
     else
         build_per_token(kb, G, R, d, S, K, k_codes, k_meta, k_resid, 0);
-    build_per_token(vb, G, R, d, S, V, v_codes, v_meta, v_resid, blocked_v(mode, kb, vb, G, d));
+    build_per_token(vb, G, R, d, S, V, v_codes, v_meta, v_resid, 0);
     return 0;
 }
 
@@ -322,11 +385,23 @@ int kvto_dequant_cache(int mode, int kb, int vb, int G, int R, int d, int cap, i
                        double* Khat, double* Vhat) {
     size_t sz[6];
     if (kvto_slice_bytes(mode, kb, vb, G, R, d, cap, sz) != 0 || S < 0 || S > cap) return -1;
+    if (blocked_v(mode, kb, vb, G, d)) {
+        uint8_t* kc = (uint8_t*)malloc((size_t)cap * 16 * kb + 1);
+        uint32_t* km = (uint32_t*)malloc((size_t)(cap / 32) * 512 + 4);
+        uint8_t* vc = (uint8_t*)malloc((size_t)cap * 16 * vb + 1);
+        uint32_t* vm = (uint32_t*)malloc((size_t)cap * 16 + 4);
+        records_load(kb, vb, kvto_n_quantized_key(mode, kb, G, R, S), kvto_n_quantized_value(mode, vb, G, R, S),
+                     k_codes, kc, km, vc, vm);
+        dequant_per_channel(kb, G, R, d, S, kc, km, k_resid, Khat);
+        dequant_per_token(vb, G, R, d, S, vc, vm, v_resid, Vhat, 1);
+        free(kc); free(km); free(vc); free(vm);
+        return 0;
+    }
     if (mode == KVTO_MODE_KIVI && kb != 16)
         dequant_per_channel(kb, G, R, d, S, k_codes, k_meta, k_resid, Khat);
     else
         dequant_per_token(kb, G, R, d, S, k_codes, k_meta, k_resid, Khat, 0);
-    dequant_per_token(vb, G, R, d, S, v_codes, v_meta, v_resid, Vhat, blocked_v(mode, kb, vb, G, d));
+    dequant_per_token(vb, G, R, d, S, v_codes, v_meta, v_resid, Vhat, 0);
     return 0;
 }
 

@@ -55,6 +55,14 @@ int32_t make_geometry(const kvt_layer_spec& s, int B, int H, int d, int cap, Geo
     r.vc = (size_t)cap * r.row_v;
     if (r.vb == 16) { r.vm = 0; r.vr = 0; }
     else { r.vm = (size_t)cap * (d / r.G) * 4; r.vr = (size_t)r.R * d * 2; }
+    if (r.v_blocked) {
+        r.rec_km = (uint32_t)(32 * r.row_k);
+        r.rec_vc = r.rec_km + 512;
+        r.rec_vm = r.rec_vc + (uint32_t)(32 * r.row_v);
+        r.rec = (size_t)r.rec_vm + 512;
+        r.kc = (size_t)(cap / 32) * r.rec;
+        r.km = r.vc = r.vm = 0;
+    }
     *g = r;
     return KVT_OK;
 }

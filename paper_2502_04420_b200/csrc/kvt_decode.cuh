@@ -202,17 +202,21 @@ struct Slice {
     const uint8_t* vc; const uint32_t* vm; const uint16_t* vr;
 };
 
-template <int KB, bool KPC>
+// REC: tile records (g.rec) — token t's key row and block meta live in record t / 32.
+template <int KB, bool KPC, bool REC = false>
 __device__ __forceinline__ void tail_k(const Slice& s, const Geometry& g, int t, int nqK, int lane, float x[4]) {
     if (t < nqK) {
-        const uint8_t* row = s.kc + (size_t)t * g.row_k;
+        const uint8_t* row = REC ? s.kc + (size_t)(t >> 5) * g.rec + (size_t)(t & 31) * g.row_k
+                                 : s.kc + (size_t)t * g.row_k;
         if constexpr (KB == 16) {
             bf16x4(reinterpret_cast<const uint16_t*>(row) + 4 * lane, x);
         } else {
             uint32_t c[4];
             codes4<KB>(row, lane, c);
             if constexpr (KPC) {
-                uint4 m = reinterpret_cast<const uint4*>(s.km + (size_t)(t / g.G) * D)[lane];
+                const uint32_t* mb = REC ? reinterpret_cast<const uint32_t*>(s.kc + (size_t)(t >> 5) * g.rec + g.rec_km)
+                                         : s.km + (size_t)(t / g.G) * D;
+                uint4 m = reinterpret_cast<const uint4*>(mb)[lane];
                 uint32_t mm[4] = {m.x, m.y, m.z, m.w};
 #pragma unroll
                 for (int i = 0; i < 4; ++i) x[i] = fmaf((float)c[i], bf2f(mm[i] & 0xffffu), bf2f(mm[i] >> 16));
@@ -228,10 +232,10 @@ __device__ __forceinline__ void tail_k(const Slice& s, const Geometry& g, int t,
     }
 }
 
-// The 4 codes of chunk (lane / 8, lane % 8) of token t in the blocked value layout.
+// The 4 codes of chunk (lane / 8, lane % 8) of token t in the blocked value layout;
+// blk = the V-code part of token t's tile record.
 template <int BITS>
-__device__ __forceinline__ void codes4_blk(const uint8_t* vc, int t, int lane, uint32_t c[4]) {
-    const uint8_t* blk = vc + (size_t)(t >> 5) * 32 * (size_t)(16 * BITS);
+__device__ __forceinline__ void codes4_blk(const uint8_t* blk, int t, int lane, uint32_t c[4]) {
     const int tau = t & 31, gam = lane >> 3, i = lane & 7;
     if constexpr (BITS == 2) {
         const uint32_t w = blk[vblk_off(2, tau, gam, i, 0)];
@@ -247,14 +251,16 @@ __device__ __forceinline__ void codes4_blk(const uint8_t* vc, int t, int lane, u
     }
 }
 
-template <int VB, bool BLK = false>
+// REC: tile records — token t's value codes (blocked) and meta live in record t / 32 of s.kc.
+template <int VB, bool REC = false>
 __device__ __forceinline__ void tail_v(const Slice& s, const Geometry& g, int t, int nqV, int lane, float x[4]) {
     if (t < nqV) {
         const uint8_t* row = s.vc + (size_t)t * g.row_v;
-        if constexpr (BLK && VB != 16) {
+        if constexpr (REC && VB != 16) {
+            const uint8_t* rec = s.kc + (size_t)(t >> 5) * g.rec;
             uint32_t c[4];
-            codes4_blk<VB>(s.vc, t, lane, c);
-            const uint32_t m = s.vm[(size_t)t * (D / g.G) + (4 * lane) / g.G];
+            codes4_blk<VB>(rec + g.rec_vc, t, lane, c);
+            const uint32_t m = reinterpret_cast<const uint32_t*>(rec + g.rec_vm + (size_t)(t & 31) * 16)[(4 * lane) / g.G];
 #pragma unroll
             for (int i = 0; i < 4; ++i) x[i] = fmaf((float)c[i], bf2f(m & 0xffffu), bf2f(m >> 16));
         } else if constexpr (VB == 16) {

@@ -332,10 +332,10 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
     const size_t bh = (size_t)b * g.H + hk;
     Slice sl;
     sl.kc = a.c.k_codes + bh * g.kc;
-    sl.km = a.c.k_meta + bh * (g.km / 4);
+    sl.km = nullptr;                                 // tile records: K meta, V codes and V meta live in kc
     sl.kr = a.c.k_resid + bh * (g.kr / 2);
-    sl.vc = a.c.v_codes + bh * g.vc;
-    sl.vm = a.c.v_meta + bh * (g.vm / 4);
+    sl.vc = nullptr;
+    sl.vm = nullptr;
     sl.vr = g.vr ? a.c.v_resid + bh * (g.vr / 2) : nullptr;
 
     const int nqK = nq_key(g.mode, g.kb, g.G, g.R, S);
@@ -349,40 +349,32 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
     bool staged = false;
     if (KVT_EXP != 5 && do_tail && n_main < S) {
         const int kq = nqK < S ? nqK : S, vq = nqV < S ? nqV : S;
-        const uint32_t b_kc = (uint32_t)(kq - n_main) * Gm::KROW;
-        const uint32_t b_km = (uint32_t)((kq - n_main + kTile - 1) / kTile) * D * 4;
+        const int q_hi = kq > vq ? kq : vq;                               // quantised tail tokens end here
+        const int r0 = n_main / kTile, r1 = (q_hi + kTile - 1) / kTile;  // their tile records
+        const uint32_t b_rec = q_hi > n_main ? (uint32_t)(r1 - r0) * Gm::STAGE : 0u;
         const uint32_t b_kr = (uint32_t)(S - kq) * D * 2;
-        const uint32_t b_vc = vq > n_main ? (uint32_t)kTile * Gm::VROW : 0u;
-        const uint32_t b_vm = (uint32_t)(vq - n_main) * 16;
         const uint32_t b_vr = (vq < S && sl.vr) ? (uint32_t)g.R * D * 2 : 0u;
-        const uint32_t total = b_kc + b_km + b_kr + b_vc + b_vm + b_vr;   // all multiples of 16
+        const uint32_t total = b_rec + b_kr + b_vr;                       // all multiples of 16
         if (Gm::SCRATCH_BYTES + total <= (uint32_t)Gm::BODY) {
             staged = true;
-            uint8_t* p = body + Gm::SCRATCH_BYTES;
-            uint8_t* p_kc = p;           uint8_t* p_km = p_kc + b_kc; uint8_t* p_kr = p_km + b_km;
-            uint8_t* p_vc = p_kr + b_kr; uint8_t* p_vm = p_vc + b_vc; uint8_t* p_vr = p_vm + b_vm;
+            uint8_t* p_rec = body + Gm::SCRATCH_BYTES;
+            uint8_t* p_kr = p_rec + b_rec;
+            uint8_t* p_vr = p_kr + b_kr;
             if (tid == 0) {
                 mbar_init(tbar);
                 asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
                 fence_proxy_async();
                 mbar_expect_tx(tbar, total);
-                if (b_kc) bulk_g2s(p_kc, sl.kc + (size_t)n_main * Gm::KROW, b_kc, tbar);
-                if (b_km) bulk_g2s(p_km, sl.km + (size_t)(n_main / kTile) * D, b_km, tbar);
+                if (b_rec) bulk_g2s(p_rec, sl.kc + (size_t)r0 * Gm::STAGE, b_rec, tbar);
                 if (b_kr) bulk_g2s(p_kr, sl.kr, b_kr, tbar);
-                if (b_vc) bulk_g2s(p_vc, sl.vc + (size_t)n_main * Gm::VROW, b_vc, tbar);
-                if (b_vm) bulk_g2s(p_vm, sl.vm + (size_t)n_main * 4, b_vm, tbar);
                 if (b_vr) bulk_g2s(p_vr, sl.vr, b_vr, tbar);
             }
-            // virtual bases: row t of the cache lands at its staged copy under the cache's own indexing
-            tl.kc = p_kc - (size_t)n_main * Gm::KROW;
-            tl.km = reinterpret_cast<const uint32_t*>(p_km) - (size_t)(n_main / kTile) * D;
+            // virtual bases: record r of the cache lands at its staged copy under the cache's own indexing
+            tl.kc = p_rec - (size_t)r0 * Gm::STAGE;
             tl.kr = reinterpret_cast<const uint16_t*>(p_kr);
-            tl.vc = p_vc - (size_t)n_main * Gm::VROW;
-            tl.vm = reinterpret_cast<const uint32_t*>(p_vm) - (size_t)n_main * 4;
             tl.vr = reinterpret_cast<const uint16_t*>(p_vr);
         }
     }
-
     // softmax heads of this thread (the QK D columns it holds after the hi/lo fold)
     const int hA = (GM == 8) ? 2 * tig : 2 * (tig & 1);
     // ---- per-head power-of-two scale of q (max |q 2^qa| in [64, 128)), computed once per CTA ----
@@ -461,7 +453,7 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
                     for (int jj = 0; jj < 8; ++jj) {
                         const int c4 = 8 * warp + ((jj + lane) & 7);             // 4-channel group index
                         float kx[4];
-                        dec::tail_k<KB, true>(tl, g, t, nqK, c4, kx);
+                        dec::tail_k<KB, true, true>(tl, g, t, nqK, c4, kx);
 #pragma unroll
                         for (int h = 0; h < GM; ++h) {
                             const float4 qv = *reinterpret_cast<const float4*>(q_s + h * D + 4 * c4);
@@ -555,7 +547,7 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
     if (staged && tid == 0) asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(tbar)));
     __syncthreads();
     KVT_STAMP(7);
-    // ---- per-warp TMA ring: lane 0 issues four bulk copies per tile onto the stage's mbarrier ----
+    // ---- per-warp TMA ring: lane 0 issues one bulk copy (the tile record) per tile onto the stage's mbarrier ----
     uint64_t* bars = reinterpret_cast<uint64_t*>(wbase + Gm::BAR_OFF);
     if (lane == 0) {
 #pragma unroll
@@ -568,10 +560,7 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
         const int t0 = (tile_lo + warp + it * kWarps) * kTile;
         uint8_t* sb = wbase + st * Gm::STAGE;
         mbar_expect_tx(bars + st, Gm::STAGE);
-        bulk_g2s(sb + Gm::K_OFF, sl.kc + (size_t)t0 * Gm::KROW, kTile * Gm::KROW, bars + st);
-        bulk_g2s(sb + Gm::KM_OFF, sl.km + (size_t)(t0 / kTile) * D, D * 4, bars + st);
-        bulk_g2s(sb + Gm::V_OFF, sl.vc + (size_t)t0 * Gm::VROW, kTile * Gm::VROW, bars + st);
-        bulk_g2s(sb + Gm::VM_OFF, sl.vm + (size_t)t0 * 4, kTile * 16, bars + st);
+        bulk_g2s(sb, sl.kc + (size_t)(t0 / kTile) * Gm::STAGE, Gm::STAGE, bars + st);   // one tile record
     };
 
     // generic-proxy writes to the ring area (tail scratch) are ordered before the first bulk copies; later

@@ -75,11 +75,22 @@ __device__ void quant_block_warp(Src src, int G, int bits, uint8_t* codes0, size
 // One per-token tensor (V, or K in per-token mode) with window R.  phase 0: quantise tokens whose
 // source is the ring (chunk 0 only); phase 1: quantise tokens from the input (all chunks);
 // phase 2: ring writes (chunk 0 only, after phase 0).
+// Token t's packed row and meta row; with tile records (g.rec) they live in the record of block t / 32
+// (codes = the record base; the row pointer is unused: the codes go to the blocked V block).
+struct TokDst {
+    uint8_t* codes; uint32_t* meta; size_t row_bytes; int gpr; size_t rec; uint32_t vc_off, vm_off;
+    __device__ uint8_t* row(int t) const { return codes + (size_t)t * row_bytes; }
+    __device__ uint32_t* meta_row(int t) const {
+        return rec ? reinterpret_cast<uint32_t*>(codes + (size_t)(t >> 5) * rec + vm_off + (size_t)(t & 31) * 16)
+                   : meta + (size_t)t * gpr;
+    }
+    __device__ uint8_t* vblk(int t) const { return rec ? codes + (size_t)(t >> 5) * rec + vc_off : nullptr; }
+};
+
 __device__ void per_token_tensor(int phase, int bits, int G, int R, int L0, int S, const uint16_t* in,
-                                 int64_t s2, uint8_t* codes, size_t row_bytes, uint32_t* meta, uint16_t* ring,
-                                 int wid, int nwarps, int lane, bool blocked = false) {
-    uint8_t* vblk = blocked ? codes : nullptr;
-    const int gpr = 128 / G;   // groups per row
+                                 int64_t s2, const TokDst& dst, uint16_t* ring, int wid, int nwarps, int lane) {
+    uint8_t* codes = dst.codes;
+    const size_t row_bytes = dst.row_bytes;
     if (bits == 16) {
         if (phase != 1) return;
         for (int t = L0 + wid; t < S; t += nwarps) {
@@ -94,13 +105,13 @@ __device__ void per_token_tensor(int phase, int bits, int G, int R, int L0, int 
         int hi = q1 < L0 ? q1 : L0;
         for (int t = q0 + wid; t < hi; t += nwarps) {
             uint2 v = reinterpret_cast<const uint2*>(ring + (size_t)(t % R) * 128)[lane];
-            quant_row_warp(v, bits, G, codes + (size_t)t * row_bytes, meta + (size_t)t * gpr, lane, vblk, t);
+            quant_row_warp(v, bits, G, dst.row(t), dst.meta_row(t), lane, dst.vblk(t), t);
         }
     } else if (phase == 1) {
         int lo = q0 > L0 ? q0 : L0;
         for (int t = lo + wid; t < q1; t += nwarps) {
             uint2 v = reinterpret_cast<const uint2*>(in + (int64_t)(t - L0) * s2)[lane];
-            quant_row_warp(v, bits, G, codes + (size_t)t * row_bytes, meta + (size_t)t * gpr, lane, vblk, t);
+            quant_row_warp(v, bits, G, dst.row(t), dst.meta_row(t), lane, dst.vblk(t), t);
         }
     } else if (R > 0) {
         int lo = (S - R) > L0 ? (S - R) : L0;
@@ -115,7 +126,7 @@ __device__ void per_token_tensor(int phase, int bits, int G, int R, int L0, int 
 // append and t - na after it.
 __device__ void per_channel_key(int phase, int bits, int G, int F, int L0, int S, const uint16_t* in, int64_t s2,
                                 uint8_t* codes, size_t row_bytes, uint32_t* meta, uint16_t* resid, int wid,
-                                int nwarps, int lane) {
+                                int nwarps, int lane, size_t rec = 0, uint32_t rec_km = 0) {
     int nb = F * (L0 / F);
     int na = F * (S / F);
     int nblk = (na - nb) / G;
@@ -129,8 +140,10 @@ __device__ void per_channel_key(int phase, int bits, int G, int F, int L0, int S
                 if (t < L0) return reinterpret_cast<const uint2*>(resid + (size_t)(t - nb) * 128);
                 return reinterpret_cast<const uint2*>(in + (int64_t)(t - L0) * s2);
             };
-            quant_block_warp(src, G, bits, codes + (size_t)t0 * row_bytes, row_bytes, meta + (size_t)(t0 / G) * 128,
-                             lane);
+            uint8_t* cblk = rec ? codes + (size_t)(t0 / G) * rec : codes + (size_t)t0 * row_bytes;
+            uint32_t* mblk = rec ? reinterpret_cast<uint32_t*>(codes + (size_t)(t0 / G) * rec + rec_km)
+                                 : meta + (size_t)(t0 / G) * 128;
+            quant_block_warp(src, G, bits, cblk, row_bytes, mblk, lane);
         }
     } else {
         int lo = na > L0 ? na : L0;
@@ -158,29 +171,32 @@ __global__ void __launch_bounds__(kWarps * 32) append_kernel(AppendArgs a) {
     uint16_t* vr = g.vr ? a.c.v_resid + bh * (g.vr / 2) : nullptr;
     const uint16_t* kin = a.k_new + (int64_t)b * a.s0 + (int64_t)h * a.s1;
     const uint16_t* vin = a.v_new + (int64_t)b * a.s0 + (int64_t)h * a.s1;
+    const TokDst kd{kc, km, g.row_k, 128 / g.G, 0, 0, 0};
+    const TokDst vd = g.rec ? TokDst{kc, nullptr, g.row_v, 128 / g.G, g.rec, g.rec_vc, g.rec_vm}
+                            : TokDst{vc, vm, g.row_v, 128 / g.G, 0, 0, 0};
 
     // phase 0 (chunk 0): residual-sourced groups; phase 1: input-sourced groups (everyone)
     if (chunk == 0) {
         if (g.key_per_channel)
-            per_channel_key(0, g.kb, g.G, g.F, L0, S, kin, a.s2, kc, g.row_k, km, kr, warp, kWarps, lane);
+            per_channel_key(0, g.kb, g.G, g.F, L0, S, kin, a.s2, kc, g.row_k, km, kr, warp, kWarps, lane, g.rec, g.rec_km);
         else
-            per_token_tensor(0, g.kb, g.G, g.R, L0, S, kin, a.s2, kc, g.row_k, km, kr, warp, kWarps, lane);
-        per_token_tensor(0, g.vb, g.G, g.R, L0, S, vin, a.s2, vc, g.row_v, vm, vr, warp, kWarps, lane, g.v_blocked);
+            per_token_tensor(0, g.kb, g.G, g.R, L0, S, kin, a.s2, kd, kr, warp, kWarps, lane);
+        per_token_tensor(0, g.vb, g.G, g.R, L0, S, vin, a.s2, vd, vr, warp, kWarps, lane);
     }
     const int wid = chunk * kWarps + warp, nw = gridDim.x * kWarps;
     if (g.key_per_channel)
-        per_channel_key(1, g.kb, g.G, g.F, L0, S, kin, a.s2, kc, g.row_k, km, kr, wid, nw, lane);
+        per_channel_key(1, g.kb, g.G, g.F, L0, S, kin, a.s2, kc, g.row_k, km, kr, wid, nw, lane, g.rec, g.rec_km);
     else
-        per_token_tensor(1, g.kb, g.G, g.R, L0, S, kin, a.s2, kc, g.row_k, km, kr, wid, nw, lane);
-    per_token_tensor(1, g.vb, g.G, g.R, L0, S, vin, a.s2, vc, g.row_v, vm, vr, wid, nw, lane, g.v_blocked);
+        per_token_tensor(1, g.kb, g.G, g.R, L0, S, kin, a.s2, kd, kr, wid, nw, lane);
+    per_token_tensor(1, g.vb, g.G, g.R, L0, S, vin, a.s2, vd, vr, wid, nw, lane);
     // phase 2 (chunk 0): new residual tokens, after every residual read of phase 0
     if (chunk == 0) {
         __syncthreads();
         if (g.key_per_channel)
-            per_channel_key(2, g.kb, g.G, g.F, L0, S, kin, a.s2, kc, g.row_k, km, kr, warp, kWarps, lane);
+            per_channel_key(2, g.kb, g.G, g.F, L0, S, kin, a.s2, kc, g.row_k, km, kr, warp, kWarps, lane, g.rec, g.rec_km);
         else
-            per_token_tensor(2, g.kb, g.G, g.R, L0, S, kin, a.s2, kc, g.row_k, km, kr, warp, kWarps, lane);
-        per_token_tensor(2, g.vb, g.G, g.R, L0, S, vin, a.s2, vc, g.row_v, vm, vr, warp, kWarps, lane, g.v_blocked);
+            per_token_tensor(2, g.kb, g.G, g.R, L0, S, kin, a.s2, kd, kr, warp, kWarps, lane);
+        per_token_tensor(2, g.vb, g.G, g.R, L0, S, vin, a.s2, vd, vr, warp, kWarps, lane);
     }
 }
 

@@ -66,9 +66,8 @@ __device__ __forceinline__ void store_packed(uint8_t* row, int lane, int bits, u
 }
 
 // Store the lane's 4-channel chunk (gam = lane / 8, i = lane % 8) of token t into the blocked value
-// layout; `codes` is the (b, h) slice base.
-__device__ __forceinline__ void store_packed_vblk(uint8_t* codes, int t, int lane, int bits, uint32_t packed) {
-    uint8_t* blk = codes + (size_t)(t >> 5) * 32 * (size_t)(16 * bits);
+// layout; `blk` is the V-code part of token t's tile record.
+__device__ __forceinline__ void store_packed_vblk(uint8_t* blk, int t, int lane, int bits, uint32_t packed) {
     const int tau = t & 31, gam = lane >> 3, i = lane & 7;
     if (bits == 2) {
         blk[vblk_off(2, tau, gam, i, 0)] = (uint8_t)packed;
@@ -81,9 +80,9 @@ __device__ __forceinline__ void store_packed_vblk(uint8_t* codes, int t, int lan
 }
 
 // Quantise one 128-channel token row held as 4 bf16 per lane; per-token groups of G channels.
-// vblk_codes != nullptr: write the codes in the blocked value layout (token t) instead of `row`.
+// vblk != nullptr: write the codes of token t into that blocked V-code block instead of `row`.
 __device__ __forceinline__ void quant_row_warp(uint2 xv, int bits, int G, uint8_t* row, uint32_t* meta_row, int lane,
-                                               uint8_t* vblk_codes = nullptr, int t = 0) {
+                                               uint8_t* vblk = nullptr, int t = 0) {
     if (bits == 16) {                                // bf16 pass-through
         reinterpret_cast<uint2*>(row)[lane] = xv;
         return;
@@ -100,7 +99,7 @@ __device__ __forceinline__ void quant_row_warp(uint2 xv, int bits, int G, uint8_
     uint32_t packed = 0;
 #pragma unroll
     for (int i = 0; i < 4; ++i) packed |= code_of(x[i], q) << (i * bits);
-    if (vblk_codes) store_packed_vblk(vblk_codes, t, lane, bits, packed);
+    if (vblk) store_packed_vblk(vblk, t, lane, bits, packed);
     else store_packed(row, lane, bits, packed);
     if ((lane & (G / 4 - 1)) == 0) meta_row[lane / (G / 4)] = q.s_bits | (q.z_bits << 16);
 }

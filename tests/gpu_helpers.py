@@ -45,7 +45,12 @@ def compare_slice(oracle, cache, spec, b, h, K_bits, V_bits, S, d=128):
     # the defined region is what §4 says it is: all code rows of quantised tokens, nothing else
     nqv = oracle.n_quantized_value(spec.mode, spec.value_bits, spec.group, spec.residual, S)
     rv = 2 * d if spec.value_bits == 16 else d * spec.value_bits // 8
-    assert int(ref["v_codes"][1].sum()) == nqv * rv
+    if cache.buffers["v_codes"] is None:        # tile records: every part of the quantised tokens in k_codes
+        nqk = oracle.n_quantized_key(spec.mode, spec.key_bits, spec.group, spec.residual, S)
+        rk = d * spec.key_bits // 8
+        assert int(ref["k_codes"][1].sum()) == nqk * rk + (nqk // 32) * d * 4 + nqv * rv + nqv * 16
+    else:
+        assert int(ref["v_codes"][1].sum()) == nqv * rv
 
 
 def rel_row_err(out, ref):

@@ -208,30 +208,38 @@ def test_o2_build_dequant_bounds(oracle, mode, kb, vb, G, R, S):
 
 
 def test_o2_meta_is_16_bytes_per_token(oracle):
-    """With G = 32, d = 128 the metadata costs 16 B per token per tensor in both modes."""
-    for mode in (0, 1):
-        sz = oracle.slice_bytes(mode, 4, 2, 32, 32, 128, 8192)
-        assert sz[1] == 8192 * 16 and sz[4] == 8192 * 16
-        assert sz[0] == 8192 * 64 and sz[3] == 8192 * 32
+    """With G = 32, d = 128 the metadata costs 16 B per token per tensor in both modes; KIVI
+    layers with quantised K and V keep all four parts in 32-token tile records inside k_codes."""
+    sz = oracle.slice_bytes(0, 4, 2, 32, 32, 128, 8192)
+    assert sz[1] == 8192 * 16 and sz[4] == 8192 * 16
+    assert sz[0] == 8192 * 64 and sz[3] == 8192 * 32
+    sz = oracle.slice_bytes(1, 4, 2, 32, 32, 128, 8192)
+    assert sz[0] == 8192 * (64 + 16 + 32 + 16) and sz[1] == sz[3] == sz[4] == 0
+    assert sz[2] == 32 * 128 * 2 and sz[5] == 32 * 128 * 2
 
 
 @pytest.mark.parametrize("vb", [2, 4, 8])
 def test_o2_blocked_value_layout_is_a_block_permutation(oracle, vb):
-    """KIVI value codes (G = 32, quantised K and V) use the blocked layout — within each
-    complete 32-token block it is a permutation of the token-major rows the per-token mode stores for
-    the same (per-token, G = 32) Eq. 2 groups; every byte of a complete block is defined."""
-    d, S = 128, 100
+    """KIVI value codes (G = 32, quantised K and V) use the blocked layout inside the tile
+    records — within each complete 32-token block it is a permutation of the token-major rows the
+    per-token mode stores for the same (per-token, G = 32) Eq. 2 groups, and the record's V meta equals
+    the per-token mode's meta rows; every byte of a complete record is defined."""
+    d, S, kb = 128, 100, 4
     K = kvt_synth.bf16_bits(kvt_synth.keys((S, d), seed=vb))
     V = kvt_synth.bf16_bits(kvt_synth.values((S, d), seed=vb + 1))
-    kivi = oracle.defined_bytes(1, 4, vb, 32, 32, d, 128, K, V)["v_codes"]
-    tm = oracle.defined_bytes(0, 4, vb, 32, 32, d, 128, K, V)["v_codes"]     # per-token, window 32: same V tokens
-    rb = d * vb // 8
+    rec_bytes, mask = oracle.defined_bytes(1, kb, vb, 32, 32, d, 128, K, V)["k_codes"]
+    tm = oracle.defined_bytes(0, 4, vb, 32, 32, d, 128, K, V)                # per-token, window 32: same V tokens
+    rk, rv = d * kb // 8, d * vb // 8
+    REC = 32 * (rk + rv) + 1024
     nqv = oracle.n_quantized_value(1, vb, 32, 32, S)                          # 68 → two complete blocks
+    nqk = oracle.n_quantized_key(1, kb, 32, 32, S)                            # 96 → three K blocks
     for blk in range(nqv // 32):
-        a = kivi[0][blk * 32 * rb:(blk + 1) * 32 * rb]
-        m = kivi[1][blk * 32 * rb:(blk + 1) * 32 * rb]
-        b = tm[0][blk * 32 * rb:(blk + 1) * 32 * rb]
-        assert m.all()
+        r = rec_bytes[blk * REC:(blk + 1) * REC]
+        assert mask[blk * REC:(blk + 1) * REC].all()
+        a = r[32 * rk + 512:32 * rk + 512 + 32 * rv]
+        b = tm["v_codes"][0][blk * 32 * rv:(blk + 1) * 32 * rv]
         assert np.array_equal(np.sort(a), np.sort(b))
         assert not np.array_equal(a, b)                                       # it is not the identity
-    assert int(kivi[1].sum()) == nqv * rb
+        assert np.array_equal(r[32 * rk + 512 + 32 * rv:], tm["v_meta"][0][blk * 32 * 16:(blk + 1) * 32 * 16])
+    # defined bytes: K rows + K meta of the quantised key blocks, V codes + meta of the quantised values
+    assert int(mask.sum()) == nqk * rk + (nqk // 32) * 512 + nqv * rv + nqv * 16
