@@ -17,8 +17,11 @@
 //     only decreases along the sequence: relative rounding 2^-12 per weight.
 //   * zero-points in fp32: bias_h = sum_c q_c z_c per key block, sum_t p_t z_(t,group) per value group.
 //
-// One warp owns whole 32-token tiles (= KIVI key blocks, G = 32) fed by its own cp.async ring (K codes,
-// K block meta, V codes with padded rows, V meta).  Thread (gid = lane/4, tig = lane%4):
+// Work: a CTA takes whole (b, kv head) units, or stream-K shares of the flattened tile space (fused merge
+// of cut units); its 4 warps take the unit's 32-token tiles (= KIVI key blocks, G = 32) round-robin, each
+// fed by its own 2-stage ring of TMA bulk copies of the tile records (K rows | K block meta | blocked V |
+// V meta); the bf16 tail tokens are staged the same way and done first, on CUDA cores.
+// Thread (gid = lane/4, tig = lane%4):
 //   QK  m-tile = 16 tokens (rows gid, gid+8), n = 8 (heads, or 4 heads x {hi, lo}), k = 16 channels;
 //       thread tig owns the 32-channel block [32 tig, 32 tig + 32) of each row (one LDS.128 at 4 bits).
 //   PV  m-tile = 16 channels of ONE value group γ (so the per-token value scale folds into B), n = 8
@@ -54,28 +57,6 @@ __device__ __forceinline__ void hmma(float d[4], uint32_t a0, uint32_t a1, uint3
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-// x >> 8 and x0 | x1 << 16 computed on the FMA pipe (IMAD.HI / IMAD) instead of the ALU pipe, which the
-// code extraction (LOP3) already saturates: the constants are made opaque so ptxas keeps the multiplies.
-// The two multipliers live in registers loaded once per thread (opaque to the optimiser).
-struct Mul { uint32_t k24, k16; };
-__device__ __forceinline__ Mul make_mul() {
-    Mul m;
-    asm volatile("mov.b32 %0, 0x01000000;" : "=r"(m.k24));
-    asm volatile("mov.b32 %0, 0x00010000;" : "=r"(m.k16));
-    return m;
-}
-#ifndef KVT_FMA_SHIFT
-#define KVT_FMA_SHIFT 0
-#endif
-#ifndef KVT_NEGF
-#define KVT_NEGF 0
-#endif
-#ifndef KVT_MINB
-#define KVT_MINB 4
-#endif
-#ifndef KVT_FIXK
-#define KVT_FIXK 0     // 1: no per-block key-scale exponent (q scaled to <= 2^3 instead)
-#endif
 #ifndef KVT_TRACE
 #define KVT_TRACE 0    // debug builds only: per-CTA (SM, start, end) timestamps for load-balance studies
 #endif
@@ -93,27 +74,8 @@ __device__ __forceinline__ Mul make_mul() {
 #define KVT_STAMP(k) do { } while (0)
 #endif
 #ifndef KVT_EXP
-#define KVT_EXP 0      // profiling experiments only: 1 = skip PV, 2 = skip QK
+#define KVT_EXP 0      // profiling experiments only: 1 = skip PV, 2 = skip QK, 3 = both, 4 = stream tiles only, 5 = no tail
 #endif
-__device__ __forceinline__ uint32_t shr8(uint32_t x, const Mul& k) {
-#if KVT_FMA_SHIFT
-    uint32_t r;
-    asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(k.k24));
-    return r;
-#else
-    return x >> 8;
-#endif
-}
-__device__ __forceinline__ uint32_t pack16(uint32_t lo, uint32_t hi, const Mul& k) {   // lo, hi < 2^16
-#if KVT_FMA_SHIFT
-    uint32_t r;
-    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(hi), "r"(k.k16), "r"(lo));
-    return r;
-#else
-    return __byte_perm(lo, hi, 0x5410);
-#endif
-}
-
 // 2^x on the SFU (MUFU.EX2, flush-to-zero). exp2f adds a subnormal range fix-up (~4 more instructions) that
 // softmax does not need: every argument here is <= 8 and results below 2^-126 are negligible against l >= 1.
 __device__ __forceinline__ float fexp2(float x) {
@@ -141,12 +103,12 @@ struct KSlots {
 };
 
 template <int KB>
-__device__ __forceinline__ uint32_t k_slot(const uint32_t* w, int m, const Mul& km) {
+__device__ __forceinline__ uint32_t k_slot(const uint32_t* w, int m) {
     if constexpr (KB == 4) {
-        const uint32_t src = (m & 2) ? shr8(w[m >> 2], km) : w[m >> 2];
+        const uint32_t src = (m & 2) ? w[m >> 2] >> 8 : w[m >> 2];
         return src & ((m & 1) ? 0x00F000F0u : 0x000F000Fu);
     } else if constexpr (KB == 2) {
-        const uint32_t src = (m & 4) ? shr8(w[m >> 3], km) : w[m >> 3];
+        const uint32_t src = (m & 4) ? w[m >> 3] >> 8 : w[m >> 3];
         return src & (0x00030003u << (2 * (m & 3)));
     } else {
         return __byte_perm(w[m >> 1], 0u, (m & 1) ? 0x4342 : 0x4140);
@@ -289,13 +251,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
-__device__ __forceinline__ void cp16(void* s, const void* g) {
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(s);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(g));
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 // One segment of a (b, kv head) unit: main tiles [tile_lo, tile_hi) (+ the tail tokens [n_main, S) when
 // do_tail).  count == 1: the segment is the whole unit and writes the output row; otherwise it leaves a
@@ -394,7 +349,7 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
     float qa_inv[2];
     {
         const int qh = (GM == 4) ? (gid & 3) : gid;
-        const int qa = (KVT_FIXK ? 3 : 7) - frexp_e(qmax_s[qh]);
+        const int qa = 7 - frexp_e(qmax_s[qh]);
 #pragma unroll
         for (int m = 0; m < 16; ++m) {
             const float sc = pow2(qa - KSlots<KB>::P(m));
@@ -402,14 +357,13 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
                                            q_s[qh * D + 32 * tig + KSlots<KB>::c1(m)] * sc));
         }
 #pragma unroll
-        for (int j = 0; j < 2; ++j) qa_inv[j] = pow2(24 - ((KVT_FIXK ? 3 : 7) - frexp_e(qmax_s[hA + j])));   // undoes 2^qa, 2^-24
+        for (int j = 0; j < 2; ++j) qa_inv[j] = pow2(24 - (7 - frexp_e(qmax_s[hA + j])));   // undoes 2^qa, 2^-24
     }
     __syncthreads();
     // GM == 4: lanes tig and tig^2 hold the same probabilities, so they prepare different value groups:
     // relative group r (0, 1) of this lane is group 2 * (tig >> 1) + r.
     const int gsh = (GM == 4) ? 2 * (tig >> 1) : 0;
     KVT_STAMP(4);
-    const Mul kmul = make_mul();
     constexpr int NGL = (GM == 4) ? 2 : 4;               // value groups prepared per lane
 
     // ---- running state ----
@@ -589,14 +543,10 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
         {
             const uint4 m4 = reinterpret_cast<const uint4*>(km_s)[lane];
             const uint32_t mw[4] = {m4.x, m4.y, m4.z, m4.w};
-#if KVT_FIXK
-            const int sbx = 0;
-#else
             // the largest scale: positive bf16 bit patterns order like their values
             uint32_t smb = max(max(mw[0] & 0xffffu, mw[1] & 0xffffu), max(mw[2] & 0xffffu, mw[3] & 0xffffu));
             smb = __reduce_max_sync(kFull, smb);                 // REDUX: one instruction for the warp max
             const int sbx = 7 - frexp_e(bf2f(smb));
-#endif
             const float ssc = pow2(sbx);
             ks_inv = pow2(-sbx);
             __half* shh = reinterpret_cast<__half*>(sh_s);
@@ -652,7 +602,6 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
         {
             const uint4* shv = reinterpret_cast<const uint4*>(sh_s + tig * Gm::SH_STRIDE);
             // GM == 4: lanes gid >= 4 carry the lo halves: b = fma(q, s, -f * hi) with f = 1 (lo) or 0 (hi)
-            const __half2 negf = __float2half2_rn((GM == 4 && gid >= 4) ? -1.0f : 0.0f);
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const uint4 s4 = shv[u];
@@ -665,11 +614,7 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
                         bq[m] = h2u(hi);
                         bq_lo[m] = h2u(__hfma2(u2h(q_h[m]), u2h(sv[e]), __hneg2(hi)));
                     } else {
-#if KVT_NEGF
-                        bq[m] = h2u(__hfma2(u2h(q_h[m]), u2h(sv[e]), __hmul2(hi, negf)));
-#else
                         bq[m] = (gid >= 4) ? h2u(__hfma2(u2h(q_h[m]), u2h(sv[e]), __hneg2(hi))) : h2u(hi);
-#endif
                     }
                 }
             }
@@ -702,8 +647,8 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
 #pragma unroll
                 for (int mt = 0; mt < 2; ++mt) {
                     float* acc = (s & 1) ? dd[mt] : de[mt];
-                    const uint32_t a0 = k_slot<KB>(w[2 * mt], 2 * s, kmul), a1 = k_slot<KB>(w[2 * mt + 1], 2 * s, kmul);
-                    const uint32_t a2 = k_slot<KB>(w[2 * mt], 2 * s + 1, kmul), a3 = k_slot<KB>(w[2 * mt + 1], 2 * s + 1, kmul);
+                    const uint32_t a0 = k_slot<KB>(w[2 * mt], 2 * s), a1 = k_slot<KB>(w[2 * mt + 1], 2 * s);
+                    const uint32_t a2 = k_slot<KB>(w[2 * mt], 2 * s + 1), a3 = k_slot<KB>(w[2 * mt + 1], 2 * s + 1);
                     hmma(acc, a0, a1, a2, a3, bq[2 * s], bq[2 * s + 1]);
                     if constexpr (GM == 8) hmma(acc, a0, a1, a2, a3, bq_lo[2 * s], bq_lo[2 * s + 1]);
                 }
@@ -960,7 +905,7 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
 __device__ __forceinline__ int cta_of(long long x, long long C, int n) { return (int)(((x + 1) * n - 1) / C); }
 
 template <int KB, int VB, int GM>
-__global__ void __launch_bounds__(kThreads, GM == 4 ? KVT_MINB : 3) decode_mma_kernel(DecodeArgs a) {
+__global__ void __launch_bounds__(kThreads, GM == 4 ? 4 : 3) decode_mma_kernel(DecodeArgs a) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ long long s_wsum[kWarps];
     __shared__ long long s_first[2];
