@@ -280,8 +280,8 @@ def run_kvt(args):
     q = [(0.5 * torch.randn(B, Hq, D, device=dev, generator=gen)).to(torch.bfloat16) for _ in range(L)]
     outs = [torch.empty(B, Hq, D, dtype=torch.bfloat16, device=dev) for _ in range(L)]
     ws_bytes = max(kvt.decode_workspace_bytes(c, Hq, [cap] * B) for c in caches)
-    ws = torch.zeros(max(ws_bytes, 16), dtype=torch.uint8, device=dev)      # split counters start at zero
-    n_combine = 0     # the tensor-core kernel merges its splits in-kernel (last CTA); see launches.csv
+    ws = torch.zeros(max(ws_bytes, 16), dtype=torch.uint8, device=dev)      # merge counters start at zero
+    n_combine = 0     # the tensor-core kernel merges cut units in-kernel (last CTA); see launches.csv
     len_before = torch.full((B,), S0, dtype=torch.int32, device=dev)
     len_after = torch.full((B,), S0 + (1 if appends else 0), dtype=torch.int32, device=dev)
     ones = torch.ones(B, dtype=torch.int32, device=dev)
@@ -408,7 +408,7 @@ def run_kvt(args):
         line = {"metric": "decode tokens/s (attention-only, mixed-precision KV)", "value": value, "unit": "tokens/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
                 "higher_is_better": True, "scaling": "strong" if seqshard else "weak", "vs_baseline": None,
-                "dtype": "fp32 (bf16 in/out)",
+                "dtype": "f32 accumulate of f16 tensor-core products (u2/u4/u8 codes, bf16 in/out)",
                 "data": "synthetic (N(0,1) K with x11 outliers on channels c%8==0, N(0,1) V, 0.5 N(0,1) q)",
                 "config": {"workload": args.workload, "layers": desc, "shape": {"L": L, "H_kv": H, "H_q": Hq, "d": D},
                            "batch_per_gpu": B, "ctx": f"{S_first}..{S_first + args.steps - 1}",

@@ -107,11 +107,43 @@ __device__ void per_token_tensor(int phase, int bits, int G, int R, int L0, int 
             uint2 v = reinterpret_cast<const uint2*>(ring + (size_t)(t % R) * 128)[lane];
             quant_row_warp(v, bits, G, dst.row(t), dst.meta_row(t), lane, dst.vblk(t), t);
         }
-    } else if (phase == 1) {
+    } else if (phase == 1 && G == 32) {
+        // 8 rows per iteration (rows t + r * nwarps), loads first, group statistics spread over the lanes
         int lo = q0 > L0 ? q0 : L0;
-        for (int t = lo + wid; t < q1; t += nwarps) {
-            uint2 v = reinterpret_cast<const uint2*>(in + (int64_t)(t - L0) * s2)[lane];
-            quant_row_warp(v, bits, G, dst.row(t), dst.meta_row(t), lane, dst.vblk(t), t);
+        for (int t = lo + wid; t < q1; t += 8 * nwarps) {
+            const int nrow = min(8, (q1 - t + nwarps - 1) / nwarps);
+            uint2 v[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r)
+                v[r] = r < nrow ? reinterpret_cast<const uint2*>(in + (int64_t)(t + r * nwarps - L0) * s2)[lane]
+                                : make_uint2(0u, 0u);
+            struct Rows {
+                const TokDst& d; int t, step;
+                __device__ uint32_t* meta_row(int r) const { return d.meta_row(t + r * step); }
+                __device__ void store(int r, int lane, int bits, uint32_t packed) const {
+                    const int tt = t + r * step;
+                    uint8_t* vb = d.vblk(tt);
+                    if (vb) quant::store_packed_vblk(vb, tt, lane, bits, packed);
+                    else quant::store_packed(d.row(tt), lane, bits, packed);
+                }
+            } rows{dst, t, nwarps};
+            quant_rows8_warp(v, nrow, bits, rows, lane);
+        }
+    } else if (phase == 1) {
+        // 4 rows per iteration, loads first: memory-level parallelism for the bulk (prefill) case
+        int lo = q0 > L0 ? q0 : L0;
+        for (int t = lo + wid; t < q1; t += 4 * nwarps) {
+            uint2 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int tt = t + u * nwarps;
+                if (tt < q1) v[u] = reinterpret_cast<const uint2*>(in + (int64_t)(tt - L0) * s2)[lane];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int tt = t + u * nwarps;
+                if (tt < q1) quant_row_warp(v[u], bits, G, dst.row(tt), dst.meta_row(tt), lane, dst.vblk(tt), tt);
+            }
         }
     } else if (R > 0) {
         int lo = (S - R) > L0 ? (S - R) : L0;
@@ -135,15 +167,21 @@ __device__ void per_channel_key(int phase, int bits, int G, int F, int L0, int S
             int t0 = nb + j * G;
             bool from_resid = t0 < L0;
             if ((phase == 0) != from_resid) continue;
-            auto src = [&](int i) -> const uint2* {
-                int t = t0 + i;
-                if (t < L0) return reinterpret_cast<const uint2*>(resid + (size_t)(t - nb) * 128);
-                return reinterpret_cast<const uint2*>(in + (int64_t)(t - L0) * s2);
-            };
             uint8_t* cblk = rec ? codes + (size_t)(t0 / G) * rec : codes + (size_t)t0 * row_bytes;
             uint32_t* mblk = rec ? reinterpret_cast<uint32_t*>(codes + (size_t)(t0 / G) * rec + rec_km)
                                  : meta + (size_t)(t0 / G) * 128;
-            quant_block_warp(src, G, bits, cblk, row_bytes, mblk, lane);
+            if (from_resid) {
+                auto src = [&](int i) -> const uint2* {
+                    int t = t0 + i;
+                    if (t < L0) return reinterpret_cast<const uint2*>(resid + (size_t)(t - nb) * 128);
+                    return reinterpret_cast<const uint2*>(in + (int64_t)(t - L0) * s2);
+                };
+                quant_block_warp(src, G, bits, cblk, row_bytes, mblk, lane);
+            } else {                               // the whole block comes from the input: strided rows
+                const uint16_t* base = in + (int64_t)(t0 - L0) * s2;
+                auto src = [&](int i) -> const uint2* { return reinterpret_cast<const uint2*>(base + (int64_t)i * s2); };
+                quant_block_warp(src, G, bits, cblk, row_bytes, mblk, lane);
+            }
         }
     } else {
         int lo = na > L0 ? na : L0;

@@ -40,7 +40,7 @@ __device__ __forceinline__ GroupQ group_params(float mn, float mx, int bits) {
     } else {
         float s32 = __fdiv_rn(__fsub_rn(mx, mn), q.qmax);
         q.s_bits = bf16_ru_bits(s32);
-        q.inv = __fdiv_rn(1.0f, bf2f(q.s_bits));
+        q.inv = __frcp_rn(bf2f(q.s_bits));               // correctly rounded 1/s (= IEEE 1.0f / s)
     }
     return q;
 }
@@ -104,6 +104,49 @@ __device__ __forceinline__ void quant_row_warp(uint2 xv, int bits, int G, uint8_
     if ((lane & (G / 4 - 1)) == 0) meta_row[lane / (G / 4)] = q.s_bits | (q.z_bits << 16);
 }
 
+
+// Eight token rows at once, G = 32: the group statistics of all 8 rows x 4 groups are spread over the 32
+// lanes (lane = group (lane / 8) of row (lane % 8)), so each lane runs the Eq. 2 scale computation (two
+// IEEE divisions) once per 8 rows instead of once per row; the codes are then formed with the row's
+// (zero-point, 1/scale) shuffled from the lane that owns it.  Same arithmetic as quant_row_warp.
+template <typename RowDst>
+__device__ __forceinline__ void quant_rows8_warp(const uint2 v[8], int nrow, int bits, const RowDst& dst, int lane) {
+    float x[8][4], mn[8], mx[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        unpack4(v[r], x[r]);
+        mn[r] = fminf(fminf(x[r][0], x[r][1]), fminf(x[r][2], x[r][3]));
+        mx[r] = fmaxf(fmaxf(x[r][0], x[r][1]), fmaxf(x[r][2], x[r][3]));
+    }
+#pragma unroll
+    for (int off = 1; off < 8; off <<= 1)
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            mn[r] = fminf(mn[r], __shfl_xor_sync(kFull, mn[r], off));
+            mx[r] = fmaxf(mx[r], __shfl_xor_sync(kFull, mx[r], off));
+        }
+    const int rr = lane & 7;
+    float mn_s = mn[0], mx_s = mx[0];
+#pragma unroll
+    for (int r = 1; r < 8; ++r)
+        if (rr == r) { mn_s = mn[r]; mx_s = mx[r]; }
+    const GroupQ q = group_params(mn_s, mx_s, bits);   // degenerate groups: inv = 0, so every code is 0
+    if (rr < nrow) dst.meta_row(rr)[lane >> 3] = q.s_bits | (q.z_bits << 16);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        if (r >= nrow) break;
+        const float inv = __shfl_sync(kFull, q.inv, (lane & 24) | r);
+        const float z = __shfl_sync(kFull, q.mn, (lane & 24) | r);
+        uint32_t packed = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            float t = rintf(__fmul_rn(__fsub_rn(x[r][i], z), inv));
+            t = fminf(fmaxf(t, 0.0f), q.qmax);
+            packed |= (uint32_t)t << (i * bits);
+        }
+        dst.store(r, lane, bits, packed);
+    }
+}
 
 }  // namespace quant
 }  // namespace kvt
