@@ -67,6 +67,10 @@ for s_, e_ in zip(sm, en):
     per.setdefault(int(s_), []).append(e_)
 cnt = np.array([len(v) for v in per.values()])
 last = np.array([max(v) for v in per.values()])
+ids = np.nonzero(keep)[0]
+for a0 in range(0, len(ids), 148):
+    seg = sm[(ids >= a0) & (ids < a0 + 148)]
+    print(f"CTAs [{a0}, {min(a0 + 148, len(ids))}): distinct SMs {len(set(seg.tolist()))} of {len(seg)}")
 print(f"SMs used {len(per)}  CTAs/SM min {cnt.min()} max {cnt.max()}  SM last-end us: min {last.min() / 1e3:.1f} median {np.median(last) / 1e3:.1f} max {last.max() / 1e3:.1f}")
 order = np.argsort(np.array(list(per.keys())))
 keys = np.array(list(per.keys()))[order]
