@@ -49,7 +49,7 @@ class _Pair(ctypes.Structure):
 
 def _load():
     if not _LIB_PATH.exists():
-        raise ImportError(f"{_LIB_PATH} is missing: build it with `python -m paper_2502_04420_b200.build` "
+        raise ImportError(f"{_LIB_PATH} is missing: build it with `python paper_2502_04420_b200/build.py` "
                           "(there is no CPU fallback)")
     lib = ctypes.CDLL(str(_LIB_PATH))
     P, i32, u64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint64
