@@ -1,6 +1,6 @@
 """Build libkvt.so in-tree: every CUDA source compiled for sm_100a only (no other arch, no PTX JIT).
 
-    python -m paper_2502_04420_b200.build [--force] [--verbose]
+    python paper_2502_04420_b200/build.py [--force] [--verbose] [--variant NAME -D MACRO=VALUE ...]
 
 Object files go to paper_2502_04420_b200/build/ and are compiled in parallel; the shared library
 is linked with the static CUDA runtime.  ptxas resource usage (-Xptxas -v) is written to
