@@ -153,7 +153,7 @@ int kvto_slice_bytes(int mode, int kb, int vb, int G, int R, int d, int cap, siz
     out[3] = (size_t)cap * row_bytes(d, vb);
     if (vb == 16) { out[4] = 0; out[5] = 0; }
     else { out[4] = (size_t)cap * (d / G) * 4; out[5] = (size_t)R * d * 2; }
-    if (mode == KVTO_MODE_KIVI && kb != 16 && vb != 16 && G == 32 && d == 128) {
+    if (kb != 16 && vb != 16 && G == 32 && d == 128) {
         /* tile records: K codes, K meta, V codes and V meta of each 32-token block are one
          * contiguous record in k_codes; k_meta, v_codes and v_meta are empty */
         out[0] = out[0] + out[1] + out[3] + out[4];
@@ -189,7 +189,8 @@ static size_t vblk_byte(int bits, int tau, int gam, int i, int k) {
 /* The blocked layout is used for KIVI layers whose key and value are both quantised, with G = 32 and
  * d = 128; every other cache keeps token-major value rows. */
 static int blocked_v(int mode, int kb, int vb, int G, int d) {
-    return mode == KVTO_MODE_KIVI && kb != 16 && vb != 16 && G == 32 && d == 128;
+    (void)mode;
+    return kb != 16 && vb != 16 && G == 32 && d == 128;
 }
 
 /* Write the packed row of token t into the blocked value layout. */
@@ -211,18 +212,23 @@ static void vblk_load(int bits, int t, const uint8_t* codes, uint8_t* row) {
                 row[(size_t)(32 * gam + 4 * i) * bits / 8 + k] = blk[vblk_byte(bits, t % 32, gam, i, k)];
 }
 
-/* Tile records, used exactly where the blocked value layout is: the k_codes slice is a
- * sequence of cap/32 records, record j holding block j (tokens 32j .. 32j+31) as
- *   [K code rows (32 x d kb/8) | K block meta (d x u32) | V codes, blocked (32 x d vb/8) | V meta (32 x 4 u32)].
+/* Tile records, used exactly where the blocked value layout is (G = 32, d = 128, 2/4/8-bit K
+ * and V, both modes): the k_codes slice is a sequence of cap/32 records, record j holding block j (tokens
+ * 32j .. 32j+31) as [K code rows (32 x d kb/8) | K meta (KIVI: d block words; per-token: 32 x 4 token
+ * words) | V codes, blocked (32 x d vb/8) | V meta (32 x 4 u32)].
  * The oracle builds the four parts as separate arrays (the same arrays the other layouts store) and moves
  * the bytes that the history defines into (out of) the records. */
 static size_t rec_bytes(int kb, int vb) { return 32 * (size_t)(16 * kb + 16 * vb) + 1024; }
 
-static void records_store(int kb, int vb, int nqK, int nqV, const uint8_t* kc, const uint32_t* km,
+static void records_store(int mode, int kb, int vb, int nqK, int nqV, const uint8_t* kc, const uint32_t* km,
                           const uint8_t* vc, const uint32_t* vm, uint8_t* rec) {
     size_t RB = rec_bytes(kb, vb), rk = (size_t)16 * kb, rv = (size_t)16 * vb;
     for (int t = 0; t < nqK; ++t) memcpy(rec + (size_t)(t / 32) * RB + (size_t)(t % 32) * rk, kc + (size_t)t * rk, rk);
-    for (int j = 0; j < nqK / 32; ++j) memcpy(rec + (size_t)j * RB + 32 * rk, km + (size_t)j * 128, 512);
+    if (mode == KVTO_MODE_KIVI)   /* K meta of block j: 128 channel words */
+        for (int j = 0; j < nqK / 32; ++j) memcpy(rec + (size_t)j * RB + 32 * rk, km + (size_t)j * 128, 512);
+    else                          /* per-token K meta: 4 group words of token t at row t mod 32 */
+        for (int t = 0; t < nqK; ++t)
+            memcpy(rec + (size_t)(t / 32) * RB + 32 * rk + (size_t)(t % 32) * 16, km + (size_t)t * 4, 16);
     for (int t = 0; t < nqV; ++t) {
         /* the blocked bytes of token t: every chunk byte of token t in block t / 32 */
         const uint8_t* blk = vc + (size_t)(t / 32) * 32 * rv;
@@ -237,11 +243,15 @@ static void records_store(int kb, int vb, int nqK, int nqV, const uint8_t* kc, c
     }
 }
 
-static void records_load(int kb, int vb, int nqK, int nqV, const uint8_t* rec, uint8_t* kc, uint32_t* km,
+static void records_load(int mode, int kb, int vb, int nqK, int nqV, const uint8_t* rec, uint8_t* kc, uint32_t* km,
                          uint8_t* vc, uint32_t* vm) {
     size_t RB = rec_bytes(kb, vb), rk = (size_t)16 * kb, rv = (size_t)16 * vb;
     for (int t = 0; t < nqK; ++t) memcpy(kc + (size_t)t * rk, rec + (size_t)(t / 32) * RB + (size_t)(t % 32) * rk, rk);
-    for (int j = 0; j < nqK / 32; ++j) memcpy(km + (size_t)j * 128, rec + (size_t)j * RB + 32 * rk, 512);
+    if (mode == KVTO_MODE_KIVI)
+        for (int j = 0; j < nqK / 32; ++j) memcpy(km + (size_t)j * 128, rec + (size_t)j * RB + 32 * rk, 512);
+    else
+        for (int t = 0; t < nqK; ++t)
+            memcpy(km + (size_t)t * 4, rec + (size_t)(t / 32) * RB + 32 * rk + (size_t)(t % 32) * 16, 16);
     for (int t = 0; t < nqV; ++t) {
         const uint8_t* src = rec + (size_t)(t / 32) * RB + 32 * rk + 512;
         uint8_t* blk = vc + (size_t)(t / 32) * 32 * rv;
@@ -317,9 +327,10 @@ int kvto_build_cache(int mode, int kb, int vb, int G, int R, int d, int cap, int
         uint32_t* km = (uint32_t*)malloc((size_t)(cap / 32) * 512 + 4);
         uint8_t* vc = (uint8_t*)malloc((size_t)cap * 16 * vb + 1);
         uint32_t* vm = (uint32_t*)malloc((size_t)cap * 16 + 4);
-        build_per_channel(kb, G, R, d, S, K, kc, km, k_resid);
+        if (mode == KVTO_MODE_KIVI) build_per_channel(kb, G, R, d, S, K, kc, km, k_resid);
+        else build_per_token(kb, G, R, d, S, K, kc, km, k_resid, 0);
         build_per_token(vb, G, R, d, S, V, vc, vm, v_resid, 1);
-        records_store(kb, vb, kvto_n_quantized_key(mode, kb, G, R, S), kvto_n_quantized_value(mode, vb, G, R, S),
+        records_store(mode, kb, vb, kvto_n_quantized_key(mode, kb, G, R, S), kvto_n_quantized_value(mode, vb, G, R, S),
                       kc, km, vc, vm, k_codes);
         free(kc); free(km); free(vc); free(vm);
         return 0;
@@ -390,9 +401,10 @@ int kvto_dequant_cache(int mode, int kb, int vb, int G, int R, int d, int cap, i
         uint32_t* km = (uint32_t*)malloc((size_t)(cap / 32) * 512 + 4);
         uint8_t* vc = (uint8_t*)malloc((size_t)cap * 16 * vb + 1);
         uint32_t* vm = (uint32_t*)malloc((size_t)cap * 16 + 4);
-        records_load(kb, vb, kvto_n_quantized_key(mode, kb, G, R, S), kvto_n_quantized_value(mode, vb, G, R, S),
+        records_load(mode, kb, vb, kvto_n_quantized_key(mode, kb, G, R, S), kvto_n_quantized_value(mode, vb, G, R, S),
                      k_codes, kc, km, vc, vm);
-        dequant_per_channel(kb, G, R, d, S, kc, km, k_resid, Khat);
+        if (mode == KVTO_MODE_KIVI) dequant_per_channel(kb, G, R, d, S, kc, km, k_resid, Khat);
+        else dequant_per_token(kb, G, R, d, S, kc, km, k_resid, Khat, 0);
         dequant_per_token(vb, G, R, d, S, vc, vm, v_resid, Vhat, 1);
         free(kc); free(km); free(vc); free(vm);
         return 0;

@@ -45,7 +45,7 @@ int32_t make_geometry(const kvt_layer_spec& s, int B, int H, int d, int cap, Geo
     r.mode = s.mode; r.kb = s.key_bits; r.vb = s.value_bits; r.G = s.group; r.R = s.residual;
     r.F = flush_size(s.group, s.residual); r.d = d; r.cap = cap; r.B = B; r.H = H;
     r.key_per_channel = (s.mode == KVT_MODE_KIVI && s.key_bits != 16);
-    r.v_blocked = (s.mode == KVT_MODE_KIVI && s.key_bits != 16 && s.value_bits != 16 && s.group == 32 && d == 128);
+    r.v_blocked = (s.key_bits != 16 && s.value_bits != 16 && s.group == 32 && d == 128);   // tile records, both modes
     r.row_k = (size_t)row_bytes(d, r.kb);
     r.row_v = (size_t)row_bytes(d, r.vb);
     r.kc = (size_t)cap * r.row_k;

@@ -17,9 +17,9 @@ KFn get_decode_k2(int VB, bool KPC, int GM);
 KFn get_decode_k4(int VB, bool KPC, int GM);
 KFn get_decode_k8(int VB, bool KPC, int GM);
 KFn get_decode_k16(int VB, bool KPC, int GM);
-KFn get_decode_mma_k2(int VB, int GM, size_t* smem);
-KFn get_decode_mma_k4(int VB, int GM, size_t* smem);
-KFn get_decode_mma_k8(int VB, int GM, size_t* smem);
+KFn get_decode_mma_k2(int VB, int GM, bool kpt, size_t* smem);
+KFn get_decode_mma_k4(int VB, int GM, bool kpt, size_t* smem);
+KFn get_decode_mma_k8(int VB, int GM, bool kpt, size_t* smem);
 
 // K3: merge n_parts partial rows [n_parts][rows][2 + D] -> out (bf16 / fp32 / partial).  One warp
 // per row; lane owns 4 channels.
@@ -81,8 +81,8 @@ static int bits_index(int b) { return b == 2 ? 0 : b == 4 ? 1 : b == 8 ? 2 : 3; 
 
 // Per-device cache of (function, smem, occupancy) for each instance; configured once.
 static std::mutex g_mu;
-static Instance g_inst[8][4][4][3][2];   // [device][kb][vb][kind: 0 generic per-token, 1 generic per-channel, 2 mma][gm]
-static bool g_ready[8][4][4][3][2];
+static Instance g_inst[8][4][4][4][2];   // [device][kb][vb][kind: 0/1 generic per-token/per-channel, 2/3 mma KIVI/per-token][gm]
+static bool g_ready[8][4][4][4][2];
 static int g_sms[8];
 
 // kind: 0 = generic CUDA-core kernel (per-token key), 1 = generic (per-channel key), 2 = tensor-core KIVI
@@ -93,11 +93,12 @@ static int32_t get_instance(int kb, int vb, int kind, int GM, Instance* out, int
     std::lock_guard<std::mutex> lk(g_mu);
     if (!g_ready[dev][ki][vi][kind][gi]) {
         Instance in;
-        if (kind == 2) {
+        if (kind >= 2) {
+            const bool kpt = kind == 3;
             switch (kb) {
-                case 2: in.fn = get_decode_mma_k2(vb, GM, &in.smem); break;
-                case 4: in.fn = get_decode_mma_k4(vb, GM, &in.smem); break;
-                default: in.fn = get_decode_mma_k8(vb, GM, &in.smem); break;
+                case 2: in.fn = get_decode_mma_k2(vb, GM, kpt, &in.smem); break;
+                case 4: in.fn = get_decode_mma_k4(vb, GM, kpt, &in.smem); break;
+                default: in.fn = get_decode_mma_k8(vb, GM, kpt, &in.smem); break;
             }
         } else {
             const bool kpc = kind == 1;
@@ -141,10 +142,10 @@ static int plan_splits(const Geometry& g, int plan_len, int occ, int sms) {
     return n;
 }
 
-// The tensor-core kernel covers exactly the caches with the blocked value layout (KIVI, G = 32, 2/4/8-bit
-// K and V); everything else runs the generic CUDA-core kernel.
+// The tensor-core kernel covers exactly the caches with tile records (G = 32, d = 128, 2/4/8-bit K and V,
+// either mode); everything else (bf16 layers, G = 64/128) runs the generic CUDA-core kernel.
 static int kernel_kind(const Geometry& g) {
-    if (g.v_blocked) return 2;
+    if (g.v_blocked) return g.key_per_channel ? 2 : 3;   // tile records: tensor-core kernel (KIVI / per-token keys)
     return g.key_per_channel ? 1 : 0;
 }
 
@@ -174,10 +175,10 @@ static int plan_ctas(const Geometry& g, int plan_len, int occ, int sms) {
 
 size_t decode_workspace(const Geometry& g, int H_q, int plan_len) {
     using namespace dec;
-    int GM = (H_q / g.H) <= 4 ? 4 : 8;
+    int GM = ((H_q / g.H) <= 4 && kernel_kind(g) != 3) ? 4 : 8;   // per-token-key tensor-core kernel: 8 columns
     Instance in; int sms = 148;
     if (get_instance(g.kb, g.vb, kernel_kind(g), GM, &in, &sms) != KVT_OK) { in.occ = 4; sms = 148; }
-    if (kernel_kind(g) == 2) {
+    if (kernel_kind(g) >= 2) {
         const int n = plan_ctas(g, plan_len, in.occ, sms);
         return n > 1 ? sk_parts_bytes(n) + counters_bytes(g) : 0;
     }
@@ -190,7 +191,7 @@ int32_t launch_decode(const Geometry& g, const CachePtrs& c, const uint16_t* q, 
                       void* stream) {
     using namespace dec;
     const int gq = H_q / g.H;
-    const int GM = gq <= 4 ? 4 : 8;
+    const int GM = (gq <= 4 && kernel_kind(g) != 3) ? 4 : 8;
     Instance in; int sms = 148;
     int32_t st = get_instance(g.kb, g.vb, kernel_kind(g), GM, &in, &sms);
     if (st) return st;
@@ -201,7 +202,7 @@ int32_t launch_decode(const Geometry& g, const CachePtrs& c, const uint16_t* q, 
     a.scale_log2 = scale * 1.4426950408889634f;
     a.out = out;
     a.final_mode = out_mode;
-    if (kind == 2) {
+    if (kind >= 2) {
         // tensor-core kernel: stream-K over all (b, kv head) units, fused merge of units cut across CTAs
         const int n = plan_ctas(g, plan_len, in.occ, sms);
         const size_t need = n > 1 ? sk_parts_bytes(n) + counters_bytes(g) : 0;

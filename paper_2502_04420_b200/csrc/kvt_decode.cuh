@@ -221,7 +221,10 @@ __device__ __forceinline__ void tail_k(const Slice& s, const Geometry& g, int t,
 #pragma unroll
                 for (int i = 0; i < 4; ++i) x[i] = fmaf((float)c[i], bf2f(mm[i] & 0xffffu), bf2f(mm[i] >> 16));
             } else {
-                uint32_t m = s.km[(size_t)t * (D / g.G) + (4 * lane) / g.G];
+                const uint32_t* mr = REC ? reinterpret_cast<const uint32_t*>(s.kc + (size_t)(t >> 5) * g.rec + g.rec_km +
+                                                                             (size_t)(t & 31) * 16)
+                                         : s.km + (size_t)t * (D / g.G);
+                uint32_t m = mr[(4 * lane) / g.G];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) x[i] = fmaf((float)c[i], bf2f(m & 0xffffu), bf2f(m >> 16));
             }

@@ -26,12 +26,21 @@ KFn get_decode_k4(int VB, bool KPC, int GM) {
     return KPC ? pick_vb<true>(VB, GM) : pick_vb<false>(VB, GM);
 }
 
-// tensor-core KIVI instances (G = 32): returns the kernel and its dynamic shared memory
-KFn get_decode_mma_k4(int VB, int GM, size_t* smem) {
+// tensor-core instances (G = 32 tile records): returns the kernel and its dynamic shared memory.
+// KPT (per-token keys) always uses the 8-column (GM = 8) form: no hi/lo split of q is needed there.
+template <int VB>
+static KFn mma_pick(int GM, bool kpt, size_t* smem) {
+    if (kpt) { *smem = mma::Geo<4, VB, 8>::SMEM; return mma::decode_mma_kernel<4, VB, 8, true>; }
+    if (GM == 4) { *smem = mma::Geo<4, VB, 4>::SMEM; return mma::decode_mma_kernel<4, VB, 4, false>; }
+    *smem = mma::Geo<4, VB, 8>::SMEM;
+    return mma::decode_mma_kernel<4, VB, 8, false>;
+}
+
+KFn get_decode_mma_k4(int VB, int GM, bool kpt, size_t* smem) {
     switch (VB) {
-        case 2: *smem = GM == 4 ? mma::Geo<4, 2, 4>::SMEM : mma::Geo<4, 2, 8>::SMEM; return GM == 4 ? mma::decode_mma_kernel<4, 2, 4> : mma::decode_mma_kernel<4, 2, 8>;
-        case 4: *smem = GM == 4 ? mma::Geo<4, 4, 4>::SMEM : mma::Geo<4, 4, 8>::SMEM; return GM == 4 ? mma::decode_mma_kernel<4, 4, 4> : mma::decode_mma_kernel<4, 4, 8>;
-        default: *smem = GM == 4 ? mma::Geo<4, 8, 4>::SMEM : mma::Geo<4, 8, 8>::SMEM; return GM == 4 ? mma::decode_mma_kernel<4, 8, 4> : mma::decode_mma_kernel<4, 8, 8>;
+        case 2: return mma_pick<2>(GM, kpt, smem);
+        case 4: return mma_pick<4>(GM, kpt, smem);
+        default: return mma_pick<8>(GM, kpt, smem);
     }
 }
 

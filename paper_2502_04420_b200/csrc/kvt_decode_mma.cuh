@@ -115,6 +115,31 @@ __device__ __forceinline__ uint32_t k_slot(const uint32_t* w, int m) {
     }
 }
 
+// Per-token keys (KPT): the scale and zero-point change per (token, 32-channel group), so k-steps must be
+// group-pure.  Slot m of lane tig holds two channels of group g = m / 4: k-steps 2g and 2g+1 then cover
+// group g alone and their accumulators are folded with that group's per-token scale.  Lane tig reads its
+// share of every group: K4 word tig of the group, K2 the (tig & 1) half of word tig / 2, K8 words 2tig, 2tig+1.
+template <int KB>
+struct KSlotsPT {
+    __host__ __device__ static constexpr int c0(int m, int tig) {
+        return KB == 4 ? 32 * (m >> 2) + 8 * tig + (m & 3)
+                       : (KB == 2 ? 32 * (m >> 2) + 16 * (tig >> 1) + 4 * (tig & 1) + (m & 3)
+                                  : 32 * (m >> 2) + 8 * tig + 4 * ((m & 3) >> 1) + 2 * (m & 1));
+    }
+    __host__ __device__ static constexpr int c1(int m, int tig) { return c0(m, tig) + (KB == 4 ? 4 : (KB == 2 ? 8 : 1)); }
+    __host__ __device__ static constexpr int P(int m) { return KB == 4 ? 4 * (m & 1) : (KB == 2 ? 2 * (m & 3) : 0); }
+};
+// w[] = the lane's words, group-major (K4: w[g]; K2: w[g] (shift by 8 for odd tig); K8: w[2g], w[2g+1])
+template <int KB>
+__device__ __forceinline__ uint32_t k_slot_pt(const uint32_t* w, int m, int tig) {
+    if constexpr (KB == 2) {
+        const uint32_t src = (tig & 1) ? w[m >> 2] >> 8 : w[m >> 2];
+        return src & (0x00030003u << (2 * (m & 3)));
+    } else {
+        return k_slot<KB>(w, m);              // K4: w[m >> 2] (shift for m & 2); K8: byte pairs of w[m >> 1]
+    }
+}
+
 // Inverse of KSlots: channel offset cc in [0, 32) -> slot * 2 + half
 template <int KB>
 __device__ __forceinline__ int k_slot_of(int cc) {
@@ -256,7 +281,7 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 // do_tail).  count == 1: the segment is the whole unit and writes the output row; otherwise it leaves a
 // partial in parts slot (cta, slot) and the last of the unit's `count` CTAs (c_first ...) merges them.
 // GM: 4 (g <= 4: n = 4 heads x {hi, lo}) or 8 (g <= 8: separate hi and lo MMAs).
-template <int KB, int VB, int GM>
+template <int KB, int VB, int GM, bool KPT>
 __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, const int b, const int hk,
                                         const int tile_lo, const int tile_hi, const bool do_tail, const int cta,
                                         const int slot, const int c_first, const int count) {
@@ -307,7 +332,8 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
         const int q_hi = kq > vq ? kq : vq;                               // quantised tail tokens end here
         const int r0 = n_main / kTile, r1 = (q_hi + kTile - 1) / kTile;  // their tile records
         const uint32_t b_rec = q_hi > n_main ? (uint32_t)(r1 - r0) * Gm::STAGE : 0u;
-        const uint32_t b_kr = (uint32_t)(S - kq) * D * 2;
+        // K residual: KIVI linear slots [0, S - nqK); per-token keys: the whole ring (slot t mod R)
+        const uint32_t b_kr = KPT ? (kq < S ? (uint32_t)g.R * D * 2 : 0u) : (uint32_t)(S - kq) * D * 2;
         const uint32_t b_vr = (vq < S && sl.vr) ? (uint32_t)g.R * D * 2 : 0u;
         const uint32_t total = b_rec + b_kr + b_vr;                       // all multiples of 16
         if (Gm::SCRATCH_BYTES + total <= (uint32_t)Gm::BODY) {
@@ -353,11 +379,31 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
 #pragma unroll
         for (int m = 0; m < 16; ++m) {
             const float sc = pow2(qa - KSlots<KB>::P(m));
-            q_h[m] = h2u(__floats2half2_rn(q_s[qh * D + 32 * tig + KSlots<KB>::c0(m)] * sc,
-                                           q_s[qh * D + 32 * tig + KSlots<KB>::c1(m)] * sc));
+            if constexpr (KPT)
+                q_h[m] = h2u(__floats2half2_rn(q_s[qh * D + KSlotsPT<KB>::c0(m, tig)] * sc,
+                                               q_s[qh * D + KSlotsPT<KB>::c1(m, tig)] * sc));
+            else
+                q_h[m] = h2u(__floats2half2_rn(q_s[qh * D + 32 * tig + KSlots<KB>::c0(m)] * sc,
+                                               q_s[qh * D + 32 * tig + KSlots<KB>::c1(m)] * sc));
         }
 #pragma unroll
         for (int j = 0; j < 2; ++j) qa_inv[j] = pow2(24 - (7 - frexp_e(qmax_s[hA + j])));   // undoes 2^qa, 2^-24
+    }
+    // per-token keys: Q_g = sum of the head's q over group g (the zero-point term sum_g z_(t,g) Q_g)
+    float qg[KPT ? 4 : 1][2];
+    if constexpr (KPT) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int gg = 0; gg < 4; ++gg) {
+                float acc = 0.0f;
+#pragma unroll
+                for (int c = 0; c < 32; c += 4) {
+                    const float4 v = *reinterpret_cast<const float4*>(q_s + (hA + j) * D + 32 * gg + c);
+                    acc += (v.x + v.y) + (v.z + v.w);
+                }
+                qg[gg][j] = acc;
+            }
     }
     __syncthreads();
     // GM == 4: lanes tig and tig^2 hold the same probabilities, so they prepare different value groups:
@@ -407,7 +453,7 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
                     for (int jj = 0; jj < 8; ++jj) {
                         const int c4 = 8 * warp + ((jj + lane) & 7);             // 4-channel group index
                         float kx[4];
-                        dec::tail_k<KB, true, true>(tl, g, t, nqK, c4, kx);
+                        dec::tail_k<KB, !KPT, true>(tl, g, t, nqK, c4, kx);
 #pragma unroll
                         for (int h = 0; h < GM; ++h) {
                             const float4 qv = *reinterpret_cast<const float4*>(q_s + h * D + 4 * c4);
@@ -538,9 +584,18 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
         const uint32_t* vm_s = reinterpret_cast<const uint32_t*>(sb + Gm::VM_OFF);
 
         // (1) key block meta: scale slots (fp16 x 2^sb) and the zero-point bias sum_c q_c z_c
-        float bias[2];
-        float ks_inv;
-        {
+        float bias[2] = {0.0f, 0.0f};
+        float ks_inv = 1.0f;
+        uint32_t mk[KPT ? 2 : 1][2][4];          // per-token keys: meta words (4 groups) of this lane's tokens
+        if constexpr (KPT) {
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    const uint4 m4 = *reinterpret_cast<const uint4*>(km_s + (16 * mt + gid + 8 * r) * 4);
+                    mk[mt][r][0] = m4.x; mk[mt][r][1] = m4.y; mk[mt][r][2] = m4.z; mk[mt][r][3] = m4.w;
+                }
+        } else {
             const uint4 m4 = reinterpret_cast<const uint4*>(km_s)[lane];
             const uint32_t mw[4] = {m4.x, m4.y, m4.z, m4.w};
             // the largest scale: positive bf16 bit patterns order like their values
@@ -598,8 +653,11 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
         }
         __syncwarp();
         // (2) B operand of QK: q_h * s_h split exactly into hi + lo
-        uint32_t bq[16], bq_lo[(GM == 8) ? 16 : 1];
-        {
+        uint32_t bq[16], bq_lo[(GM == 8 && !KPT) ? 16 : 1];
+        if constexpr (KPT) {
+#pragma unroll
+            for (int m = 0; m < 16; ++m) bq[m] = q_h[m];   // q (bf16) is exact in fp16: no scale, no lo half
+        } else {
             const uint4* shv = reinterpret_cast<const uint4*>(sh_s + tig * Gm::SH_STRIDE);
             // GM == 4: lanes gid >= 4 carry the lo halves: b = fma(q, s, -f * hi) with f = 1 (lo) or 0 (hi)
 #pragma unroll
@@ -610,7 +668,7 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
                 for (int e = 0; e < 4; ++e) {
                     const int m = 4 * u + e;
                     const __half2 hi = __hmul2(u2h(q_h[m]), u2h(sv[e]));
-                    if constexpr (GM == 8) {
+                    if constexpr (GM == 8 && !KPT) {
                         bq[m] = h2u(hi);
                         bq_lo[m] = h2u(__hfma2(u2h(q_h[m]), u2h(sv[e]), __hneg2(hi)));
                     } else {
@@ -621,7 +679,48 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
         }
         // (3) QK on the tensor cores: two m-tiles of 16 tokens, 4 independent accumulator chains
         float dq[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
-        if (KVT_EXP != 2 && KVT_EXP != 3) {
+        if constexpr (KPT) {
+            // per-token keys: group-pure k-step pairs; dq = sum_g s_(t,g) D_g 2^(24-qa) + z_(t,g) Q_g
+            uint32_t w[4][KB == 2 ? 4 : KB];   // rows gid, gid+8, 16+gid, 24+gid; the lane's words of each group
+#pragma unroll
+            for (int rr = 0; rr < 4; ++rr) {
+                const uint8_t* r0 = kc_s + (8 * rr + gid) * Gm::KROW;
+#pragma unroll
+                for (int gg = 0; gg < 4; ++gg) {
+                    if constexpr (KB == 4) {
+                        w[rr][gg] = *reinterpret_cast<const uint32_t*>(r0 + 16 * gg + 4 * tig);
+                    } else if constexpr (KB == 2) {
+                        w[rr][gg] = *reinterpret_cast<const uint32_t*>(r0 + 8 * gg + 4 * (tig >> 1));
+                    } else {
+                        const uint2 x = *reinterpret_cast<const uint2*>(r0 + 32 * gg + 8 * tig);
+                        w[rr][2 * gg] = x.x; w[rr][2 * gg + 1] = x.y;
+                    }
+                }
+            }
+#pragma unroll
+            for (int gg = 0; gg < 4; ++gg) {
+                float acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+#pragma unroll
+                for (int s2 = 0; s2 < 2; ++s2) {
+                    const int s = 2 * gg + s2;
+#pragma unroll
+                    for (int mt = 0; mt < 2; ++mt) {
+                        const uint32_t a0 = k_slot_pt<KB>(w[2 * mt], 2 * s, tig), a1 = k_slot_pt<KB>(w[2 * mt + 1], 2 * s, tig);
+                        const uint32_t a2 = k_slot_pt<KB>(w[2 * mt], 2 * s + 1, tig);
+                        const uint32_t a3 = k_slot_pt<KB>(w[2 * mt + 1], 2 * s + 1, tig);
+                        hmma(acc[mt], a0, a1, a2, a3, bq[2 * s], bq[2 * s + 1]);
+                    }
+                }
+#pragma unroll
+                for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const uint32_t mw = mk[mt][i >> 1][gg];
+                        dq[mt][i] = fmaf(bf2f(mw & 0xffffu) * qa_inv[i & 1], acc[mt][i],
+                                         fmaf(bf2f(mw >> 16), qg[gg][i & 1], dq[mt][i]));
+                    }
+            }
+        } else if (KVT_EXP != 2 && KVT_EXP != 3) {
             uint32_t w[4][KB];        // rows gid, gid+8, 16+gid, 24+gid
 #pragma unroll
             for (int rr = 0; rr < 4; ++rr) {
@@ -667,8 +766,8 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
         bool resc = false;
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-            const float cs = a.scale_log2 * qa_inv[j] * ks_inv;
-            const float cb = a.scale_log2 * bias[j];
+            const float cs = KPT ? a.scale_log2 : a.scale_log2 * qa_inv[j] * ks_inv;   // KPT: dq holds q.k
+            const float cb = KPT ? 0.0f : a.scale_log2 * bias[j];
             float l4[4];
             l4[0] = fmaf(dq[0][j], cs, cb);
             l4[1] = fmaf(dq[0][2 + j], cs, cb);
@@ -904,7 +1003,7 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
 // the CTA whose range [c C / n, (c + 1) C / n) holds position x
 __device__ __forceinline__ int cta_of(long long x, long long C, int n) { return (int)(((x + 1) * n - 1) / C); }
 
-template <int KB, int VB, int GM>
+template <int KB, int VB, int GM, bool KPT>
 __global__ void __launch_bounds__(kThreads, GM == 4 ? 4 : 3) decode_mma_kernel(DecodeArgs a) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ long long s_wsum[kWarps];
@@ -957,7 +1056,7 @@ __global__ void __launch_bounds__(kThreads, GM == 4 ? 4 : 3) decode_mma_kernel(D
         const int x0 = (int)(pos - Pu);
         const int x1 = (int)(hi - Pu < uc.cost ? hi - Pu : uc.cost);
         const int cf = cta_of(Pu, C, n), cl = cta_of(Pu + uc.cost - 1, C, n);
-        segment<KB, VB, GM>(a, smem, b, hk, min(x0, uc.tiles), min(x1, uc.tiles), x1 == uc.cost, cta,
+        segment<KB, VB, GM, KPT>(a, smem, b, hk, min(x0, uc.tiles), min(x1, uc.tiles), x1 == uc.cost, cta,
                             cta == cf ? 1 : 0, cf, cl - cf + 1);
         pos = Pu + x1;
         __syncthreads();                                    // the next segment reuses shared memory

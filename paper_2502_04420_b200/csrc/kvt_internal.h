@@ -51,11 +51,12 @@ __host__ __device__ inline uint32_t vblk_off(int bits, int tau, int gam, int i, 
 struct Geometry {
     int mode, kb, vb, G, R, F, d, cap, B, H;
     bool key_per_channel;          // KIVI key with bits < 16
-    bool v_blocked;                // tile records + blocked value layout (KIVI, K and V quantised, G = 32, d = 128; §4)
+    bool v_blocked;                // tile records + blocked value layout (K and V quantised, G = 32, d = 128; §4)
     size_t row_k, row_v;           // bytes per token row
     size_t kc, km, kr, vc, vm, vr; // bytes per (b,h) slice
     // tile records (v_blocked): k_codes holds cap/32 records of `rec` bytes, record j = block j as
-    // [K code rows | K block meta (at rec_km) | V codes, blocked (at rec_vc) | V meta (at rec_vm)]
+    // [K code rows | K meta (at rec_km: KIVI block words, or per-token rows of 4 words) | V codes, blocked
+    // (at rec_vc) | V meta (at rec_vm)]
     size_t rec;
     uint32_t rec_km, rec_vc, rec_vm;
 };

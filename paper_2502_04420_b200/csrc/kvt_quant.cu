@@ -77,14 +77,17 @@ __device__ void quant_block_warp(Src src, int G, int bits, uint8_t* codes0, size
 // phase 2: ring writes (chunk 0 only, after phase 0).
 // Token t's packed row and meta row; with tile records (g.rec) they live in the record of block t / 32
 // (codes = the record base; the row pointer is unused: the codes go to the blocked V block).
+// With tile records: rows at blk_off == 0 are token-major code rows (K), otherwise the blocked V block.
 struct TokDst {
-    uint8_t* codes; uint32_t* meta; size_t row_bytes; int gpr; size_t rec; uint32_t vc_off, vm_off;
-    __device__ uint8_t* row(int t) const { return codes + (size_t)t * row_bytes; }
+    uint8_t* codes; uint32_t* meta; size_t row_bytes; int gpr; size_t rec; uint32_t blk_off, meta_off;
+    __device__ uint8_t* row(int t) const {
+        return rec ? codes + (size_t)(t >> 5) * rec + (size_t)(t & 31) * row_bytes : codes + (size_t)t * row_bytes;
+    }
     __device__ uint32_t* meta_row(int t) const {
-        return rec ? reinterpret_cast<uint32_t*>(codes + (size_t)(t >> 5) * rec + vm_off + (size_t)(t & 31) * 16)
+        return rec ? reinterpret_cast<uint32_t*>(codes + (size_t)(t >> 5) * rec + meta_off + (size_t)(t & 31) * 16)
                    : meta + (size_t)t * gpr;
     }
-    __device__ uint8_t* vblk(int t) const { return rec ? codes + (size_t)(t >> 5) * rec + vc_off : nullptr; }
+    __device__ uint8_t* vblk(int t) const { return rec && blk_off ? codes + (size_t)(t >> 5) * rec + blk_off : nullptr; }
 };
 
 __device__ void per_token_tensor(int phase, int bits, int G, int R, int L0, int S, const uint16_t* in,
@@ -209,7 +212,8 @@ __global__ void __launch_bounds__(kWarps * 32) append_kernel(AppendArgs a) {
     uint16_t* vr = g.vr ? a.c.v_resid + bh * (g.vr / 2) : nullptr;
     const uint16_t* kin = a.k_new + (int64_t)b * a.s0 + (int64_t)h * a.s1;
     const uint16_t* vin = a.v_new + (int64_t)b * a.s0 + (int64_t)h * a.s1;
-    const TokDst kd{kc, km, g.row_k, 128 / g.G, 0, 0, 0};
+    const TokDst kd = g.rec ? TokDst{kc, nullptr, g.row_k, 128 / g.G, g.rec, 0, g.rec_km}   // per-token K rows in records
+                            : TokDst{kc, km, g.row_k, 128 / g.G, 0, 0, 0};
     const TokDst vd = g.rec ? TokDst{kc, nullptr, g.row_v, 128 / g.G, g.rec, g.rec_vc, g.rec_vm}
                             : TokDst{vc, vm, g.row_v, 128 / g.G, 0, 0, 0};
 

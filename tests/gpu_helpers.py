@@ -48,7 +48,8 @@ def compare_slice(oracle, cache, spec, b, h, K_bits, V_bits, S, d=128):
     if cache.buffers["v_codes"] is None:        # tile records: every part of the quantised tokens in k_codes
         nqk = oracle.n_quantized_key(spec.mode, spec.key_bits, spec.group, spec.residual, S)
         rk = d * spec.key_bits // 8
-        assert int(ref["k_codes"][1].sum()) == nqk * rk + (nqk // 32) * d * 4 + nqv * rv + nqv * 16
+        kmeta = (nqk // 32) * d * 4 if spec.mode == oracle.MODE_KIVI else nqk * (d // spec.group) * 4
+        assert int(ref["k_codes"][1].sum()) == nqk * rk + kmeta + nqv * rv + nqv * 16
     else:
         assert int(ref["v_codes"][1].sum()) == nqv * rv
 

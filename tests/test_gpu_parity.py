@@ -32,6 +32,9 @@ def kvt():
 
 SPECS = [
     ("pt_k8v4_g32", lambda k: k.LayerSpec.per_token(8, 4)),
+    ("pt_k4v2_r32", lambda k: k.LayerSpec.per_token(4, 2, residual=32)),     # per-token key ring residual
+    ("pt_k2v4", lambda k: k.LayerSpec.per_token(2, 4)),
+    ("pt_k8v8_r64", lambda k: k.LayerSpec.per_token(8, 8, residual=64)),
     ("pt_k2v2_g64", lambda k: k.LayerSpec.per_token(2, 2, group=64)),
     ("pt_k4v8_g128_r32", lambda k: k.LayerSpec.per_token(4, 8, group=128, residual=32)),
     ("kivi_k4v2", lambda k: k.LayerSpec.kivi(4, 2)),

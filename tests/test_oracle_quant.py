@@ -208,14 +208,16 @@ def test_o2_build_dequant_bounds(oracle, mode, kb, vb, G, R, S):
 
 
 def test_o2_meta_is_16_bytes_per_token(oracle):
-    """With G = 32, d = 128 the metadata costs 16 B per token per tensor in both modes; KIVI
-    layers with quantised K and V keep all four parts in 32-token tile records inside k_codes."""
-    sz = oracle.slice_bytes(0, 4, 2, 32, 32, 128, 8192)
-    assert sz[1] == 8192 * 16 and sz[4] == 8192 * 16
+    """With G = 32, d = 128 the metadata costs 16 B per token per tensor in both modes; with
+    quantised K and V (either mode) all four parts live in 32-token tile records inside k_codes; other
+    layouts (G = 64 here) keep four separate buffers."""
+    for mode in (0, 1):
+        sz = oracle.slice_bytes(mode, 4, 2, 32, 32, 128, 8192)
+        assert sz[0] == 8192 * (64 + 16 + 32 + 16) and sz[1] == sz[3] == sz[4] == 0
+        assert sz[2] == 32 * 128 * 2 and sz[5] == 32 * 128 * 2
+    sz = oracle.slice_bytes(0, 4, 2, 64, 32, 128, 8192)
+    assert sz[1] == 8192 * 8 and sz[4] == 8192 * 8
     assert sz[0] == 8192 * 64 and sz[3] == 8192 * 32
-    sz = oracle.slice_bytes(1, 4, 2, 32, 32, 128, 8192)
-    assert sz[0] == 8192 * (64 + 16 + 32 + 16) and sz[1] == sz[3] == sz[4] == 0
-    assert sz[2] == 32 * 128 * 2 and sz[5] == 32 * 128 * 2
 
 
 @pytest.mark.parametrize("vb", [2, 4, 8])
@@ -228,7 +230,8 @@ def test_o2_blocked_value_layout_is_a_block_permutation(oracle, vb):
     K = kvt_synth.bf16_bits(kvt_synth.keys((S, d), seed=vb))
     V = kvt_synth.bf16_bits(kvt_synth.values((S, d), seed=vb + 1))
     rec_bytes, mask = oracle.defined_bytes(1, kb, vb, 32, 32, d, 128, K, V)["k_codes"]
-    tm = oracle.defined_bytes(0, 4, vb, 32, 32, d, 128, K, V)                # per-token, window 32: same V tokens
+    # token-major reference: per-token mode, window 32 (same V tokens), bf16 keys (so no tile records)
+    tm = oracle.defined_bytes(0, 16, vb, 32, 32, d, 128, K, V)
     rk, rv = d * kb // 8, d * vb // 8
     REC = 32 * (rk + rv) + 1024
     nqv = oracle.n_quantized_value(1, vb, 32, 32, S)                          # 68 → two complete blocks
