@@ -32,6 +32,8 @@ WORKLOADS = {
     "llama-3.25": ("configs/llama-3.1-8b_kivi_3.25.json", (32, 8, 32), 64, 8192),
     "qwen-4.00": ("configs/qwen2.5-7b_per-token-asym_4.00.json", (28, 4, 28), 64, 8192),
     "qwen-3.92": ("configs/qwen2.5-7b_kivi_3.92.json", (28, 4, 28), 64, 8192),
+    # the paper's exact 4.00 map in its own mode (per-token-asym, G = 32, R = 0), not the KIVI layout of A19
+    "qwen-4.00-pertoken": ("configs/qwen2.5-7b_per-token-asym_4.00.json", (28, 4, 28), 64, 8192),
     "llama-kv8": (None, (32, 8, 32), 64, 8192),
     "qwen-kv8": (None, (28, 4, 28), 64, 8192),
     # config 5: 128k context, sequence-sharded over the ranks (partial -> NCCL all-gather -> combine)
