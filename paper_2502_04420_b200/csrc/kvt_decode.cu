@@ -175,7 +175,7 @@ static int plan_ctas(const Geometry& g, int plan_len, int occ, int sms) {
 
 size_t decode_workspace(const Geometry& g, int H_q, int plan_len) {
     using namespace dec;
-    int GM = ((H_q / g.H) <= 4 && kernel_kind(g) != 3) ? 4 : 8;   // per-token-key tensor-core kernel: 8 columns
+    int GM = (H_q / g.H) <= 4 ? 4 : 8;
     Instance in; int sms = 148;
     if (get_instance(g.kb, g.vb, kernel_kind(g), GM, &in, &sms) != KVT_OK) { in.occ = 4; sms = 148; }
     if (kernel_kind(g) >= 2) {
@@ -191,7 +191,7 @@ int32_t launch_decode(const Geometry& g, const CachePtrs& c, const uint16_t* q, 
                       void* stream) {
     using namespace dec;
     const int gq = H_q / g.H;
-    const int GM = (gq <= 4 && kernel_kind(g) != 3) ? 4 : 8;
+    const int GM = gq <= 4 ? 4 : 8;
     Instance in; int sms = 148;
     int32_t st = get_instance(g.kb, g.vb, kernel_kind(g), GM, &in, &sms);
     if (st) return st;

@@ -27,9 +27,11 @@ KFn get_decode_k2(int VB, bool KPC, int GM) {
 }
 
 // tensor-core instances (G = 32 tile records): returns the kernel and its dynamic shared memory.
-// KPT (per-token keys) always uses the 8-column (GM = 8) form: no hi/lo split of q is needed there.
+// KPT (per-token keys): q needs no hi/lo split, so with g <= 4 the 8 columns hold the 4 heads twice (the
+// lanes tig and tig ^ 2 then see the same heads, as after the KIVI hi/lo fold).
 template <int VB>
 static KFn mma_pick(int GM, bool kpt, size_t* smem) {
+    if (kpt && GM == 4) { *smem = mma::Geo<2, VB, 4>::SMEM; return mma::decode_mma_kernel<2, VB, 4, true>; }
     if (kpt) { *smem = mma::Geo<2, VB, 8>::SMEM; return mma::decode_mma_kernel<2, VB, 8, true>; }
     if (GM == 4) { *smem = mma::Geo<2, VB, 4>::SMEM; return mma::decode_mma_kernel<2, VB, 4, false>; }
     *smem = mma::Geo<2, VB, 8>::SMEM;

@@ -656,7 +656,8 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
         uint32_t bq[16], bq_lo[(GM == 8 && !KPT) ? 16 : 1];
         if constexpr (KPT) {
 #pragma unroll
-            for (int m = 0; m < 16; ++m) bq[m] = q_h[m];   // q (bf16) is exact in fp16: no scale, no lo half
+            for (int m = 0; m < 16; ++m) bq[m] = q_h[m];   // q (bf16) is exact in fp16: no lo half (GM = 4: the
+                                                            // 8 columns hold heads gid & 3, i.e. the 4 heads twice)
         } else {
             const uint4* shv = reinterpret_cast<const uint4*>(sh_s + tig * Gm::SH_STRIDE);
             // GM == 4: lanes gid >= 4 carry the lo halves: b = fma(q, s, -f * hi) with f = 1 (lo) or 0 (hi)
