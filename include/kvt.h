@@ -178,6 +178,39 @@ int32_t kvt_layer_sensitivity(int32_t mode, int32_t group, int32_t residual,
                               const kvt_pair* pairs, int32_t n_pairs, kvt_errors* out_dev,
                               void* workspace, uint64_t ws_bytes, void* stream);
 
+/* ---- search-space pruning after calibration (host only, no CUDA) -----------------------------------
+ * The step after a7: the per-layer profiles e_o[layer][pair] (from kvt_layer_sensitivity, averaged over
+ * the calibration prompts by the caller, A14) become the reduced search space S_p^G of the offline MOO
+ * search (App. D).  Readings A24-A27.  All buffers are HOST memory
+ * owned by the caller; nothing is retained between calls. */
+
+/* Intra-layer pruning: keep[i] = 1 iff pair i is on the Pareto frontier of (equivalent bits
+ * (b_k + b_v)/2, e_o[i]), i.e. no j has bits_j <= bits_i and e_o[j] <= e_o[i] with one of them strict;
+ * exact ties both survive (A24).  pairs/e_o/keep: [n_pairs], n_pairs >= 1.
+ * Errors: KVT_ERR_INVALID_ARG for null pointers, n_pairs < 1, bits outside {2,4,8,16}, non-finite e_o. */
+int32_t kvt_pareto_prune(const kvt_pair* pairs, const double* e_o, int32_t n_pairs, uint8_t* keep);
+
+/* DBSCAN (Ester et al. 1996, the clustering of App. D): points [n][dim] row-major; neighbourhood =
+ * Euclidean distance <= eps, the point itself included; core = >= min_samples neighbours; clusters are
+ * grown from unlabelled core points in index order, a border point joins the first cluster that reaches
+ * it.  labels[n] = cluster id (0, 1, ... in order of discovery) or -1 for noise (A25).
+ * Errors: KVT_ERR_INVALID_ARG for n < 0, dim < 1, min_samples < 1, eps < 0 or non-finite input. */
+int32_t kvt_dbscan(const double* points, int32_t n, int32_t dim, double eps, int32_t min_samples,
+                   int32_t* labels);
+
+/* The two-level pruning of P:316-325: per layer kvt_pareto_prune over the common candidate list
+ * `pairs` (e_o: [n_layers][n_pairs]); layers partitioned by identical kept sets; inside each
+ * partition kvt_dbscan(eps, min_samples) on each layer's e_o over the partition's kept pairs (
+ * the paper uses eps = 0.05, min_samples = 2); DBSCAN noise layers become singleton groups (A26).
+ * Outputs: keep [n_layers][n_pairs]; group_of_layer [n_layers] with groups numbered 0..G-1 in order of
+ * their first layer (A27); *n_groups = G.  Requires 1 <= n_pairs <= 64, n_layers >= 1. */
+int32_t kvt_prune_and_cluster(const kvt_pair* pairs, int32_t n_pairs, const double* e_o, int32_t n_layers,
+                              double eps, int32_t min_samples, uint8_t* keep, int32_t* group_of_layer,
+                              int32_t* n_groups);
+
+/* log10 of the search-space size prod_i counts[i] ("9^L", "5^G = 15625"); counts >= 1. */
+int32_t kvt_search_space_log10(const int32_t* counts, int32_t n, double* log10_size);
+
 #ifdef __cplusplus
 }
 #endif

@@ -76,6 +76,11 @@ def _load():
         "kvt_sensitivity_workspace_bytes": (i32, [i32, i32, i32, i32, i32, i32, ctypes.POINTER(u64)]),
         "kvt_layer_sensitivity": (i32, [i32, i32, i32, P, i32, i32, i32, P, P, i32, i32, i32, ctypes.c_float,
                                         ctypes.POINTER(_Pair), i32, P, P, u64, P]),
+        "kvt_pareto_prune": (i32, [ctypes.POINTER(_Pair), P, i32, P]),
+        "kvt_dbscan": (i32, [P, i32, i32, ctypes.c_double, i32, P]),
+        "kvt_prune_and_cluster": (i32, [ctypes.POINTER(_Pair), i32, P, i32, ctypes.c_double, i32, P, P,
+                                        ctypes.POINTER(i32)]),
+        "kvt_search_space_log10": (i32, [P, i32, ctypes.POINTER(ctypes.c_double)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -90,7 +95,8 @@ EXPORTED = ("kvt_abi_version", "kvt_status_string", "kvt_last_error", "kvt_confi
             "kvt_config_layer", "kvt_config_equivalent_bits", "kvt_config_label_bits", "kvt_config_model_name",
             "kvt_config_free", "kvt_validate_spec", "kvt_cache_buffer_sizes", "kvt_quantize_append",
             "kvt_decode_workspace_bytes", "kvt_decode_attention", "kvt_decode_attention_partial",
-            "kvt_combine_partials", "kvt_sensitivity_workspace_bytes", "kvt_layer_sensitivity")
+            "kvt_combine_partials", "kvt_sensitivity_workspace_bytes", "kvt_layer_sensitivity",
+            "kvt_pareto_prune", "kvt_dbscan", "kvt_prune_and_cluster", "kvt_search_space_log10")
 
 
 def lib():
@@ -331,3 +337,62 @@ def layer_sensitivity(mode: int, group: int, residual: int, q: torch.Tensor, k: 
                                       d, float(scale), cp, len(pairs), _ptr(out), _ptr(ws), ws.numel(),
                                       ctypes.c_void_p(_stream(stream))))
     return out
+
+
+# ------------------------------------------------------------------------------------------------
+# search-space pruning after calibration (host only): App. D
+# ------------------------------------------------------------------------------------------------
+def _pairs(pairs: Sequence[tuple]):
+    return (_Pair * len(pairs))(*[_Pair(int(a), int(b)) for a, b in pairs])
+
+
+def _f64(a) -> "np.ndarray":
+    import numpy as np
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def pareto_prune(pairs: Sequence[tuple], e_o) -> list:
+    """Intra-layer pruning: True for the pairs on the (equivalent bits, e_o) Pareto frontier."""
+    import numpy as np
+    e = _f64(e_o)
+    if e.shape != (len(pairs),):
+        raise ValueError("e_o must have one entry per pair")
+    keep = np.zeros(len(pairs), dtype=np.uint8)
+    _check(_lib.kvt_pareto_prune(_pairs(pairs), e.ctypes.data, len(pairs), keep.ctypes.data))
+    return [bool(x) for x in keep]
+
+
+def dbscan(points, eps: float = 0.05, min_samples: int = 2) -> list:
+    """DBSCAN labels (cluster ids in order of discovery, -1 = noise) of points [n][dim] (App. D)."""
+    import numpy as np
+    x = _f64(points)
+    if x.ndim != 2:
+        raise ValueError("points must be [n][dim]")
+    lab = np.zeros(x.shape[0], dtype=np.int32)
+    _check(_lib.kvt_dbscan(x.ctypes.data, x.shape[0], x.shape[1], float(eps), int(min_samples), lab.ctypes.data))
+    return [int(v) for v in lab]
+
+
+def prune_and_cluster(pairs: Sequence[tuple], e_o, eps: float = 0.05, min_samples: int = 2):
+    """Two-level search-space pruning: e_o [L][n_pairs] -> (keep [L][n_pairs] bool,
+    group_of_layer [L], n_groups)."""
+    import numpy as np
+    e = _f64(e_o)
+    if e.ndim != 2 or e.shape[1] != len(pairs):
+        raise ValueError("e_o must be [n_layers][n_pairs]")
+    L = e.shape[0]
+    keep = np.zeros((L, len(pairs)), dtype=np.uint8)
+    grp = np.zeros(L, dtype=np.int32)
+    ng = ctypes.c_int32()
+    _check(_lib.kvt_prune_and_cluster(_pairs(pairs), len(pairs), e.ctypes.data, L, float(eps), int(min_samples),
+                                      keep.ctypes.data, grp.ctypes.data, ctypes.byref(ng)))
+    return keep.astype(bool), [int(g) for g in grp], int(ng.value)
+
+
+def search_space_log10(counts: Sequence[int]) -> float:
+    """log10 of prod(counts): the search-space size S^L or S_p^G."""
+    import numpy as np
+    c = np.ascontiguousarray(np.asarray(counts, dtype=np.int32))
+    out = ctypes.c_double()
+    _check(_lib.kvt_search_space_log10(c.ctypes.data, c.size, ctypes.byref(out)))
+    return float(out.value)
