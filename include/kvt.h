@@ -50,7 +50,11 @@ typedef enum {
  *   KIVI:           K per channel in token blocks of `group` with a full-precision residual of up to
  *                   `residual` tokens flushed block-wise; V per token in channel groups with a
  *                   sliding full-precision window of `residual` tokens (R = G = 32; A7, A8). */
-typedef enum { KVT_MODE_PER_TOKEN_ASYM = 0, KVT_MODE_KIVI = 1 } kvt_mode;
+typedef enum { KVT_MODE_PER_TOKEN_ASYM = 0, KVT_MODE_KIVI = 1,
+               /* kvt_layer_sensitivity only (not a cache layout): K and V quantised per channel with
+                * statistics over the whole trace (T-Mode; A28).  Whole-sequence statistics cannot be
+                * appended write-once, so kvt_config_load rejects it. */
+               KVT_MODE_PER_CHANNEL_ASYM = 2 } kvt_mode;
 
 /* One layer's precision pair (P_k, P_v) (candidates {2,4,8}^2 P:316; 16 = bf16). */
 typedef struct { int32_t key_bits, value_bits; } kvt_pair;
@@ -163,7 +167,8 @@ int32_t kvt_combine_partials(const float* gathered, int32_t n_shards, int32_t ba
 
 /* ---- a7: layer sensitivity (App. B protocol P:622-623) -------------------------------
  * For one layer and one calibration prompt, for every pair p: quantise the whole trace statically
- * at (b_k, b_v) under (mode, group, residual) (A15), run the t_q decode queries causally (query i at
+ * at (b_k, b_v) under (mode, group, residual) (A15; mode KVT_MODE_PER_CHANNEL_ASYM: one group per channel
+ * column of the whole trace for K and V, `group` ignored, residual must be 0, A28), run the t_q decode queries causally (query i at
  * position q_pos0 + i attends to tokens [0, q_pos0 + i]) with (K, V) and with (K_hat, V_hat), and
  * write fp64 out_dev[p] = {e_k, e_v, e_a, e_o, e_o_l1} (A13, A16).  Arithmetic is fp64.
  *   q: bf16 [H_q][T_q][d]; k, v: bf16 [H_kv][S][d]; pairs: HOST array; out_dev: device. */

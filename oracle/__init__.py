@@ -28,7 +28,8 @@ _LIB = _HERE / "libkvt_oracle.so"
 
 MODE_PER_TOKEN = 0
 MODE_KIVI = 1
-MODES = {"per-token-asym": MODE_PER_TOKEN, "kivi": MODE_KIVI}
+MODE_PER_CHANNEL = 2        # sensitivity only (A28)
+MODES = {"per-token-asym": MODE_PER_TOKEN, "kivi": MODE_KIVI, "per-channel-asym": MODE_PER_CHANNEL}
 
 
 def build(force: bool = False) -> Path:

@@ -451,6 +451,23 @@ void kvto_attention(const uint16_t* q, int g, const double* Khat, const double* 
 /* ------------------------------------------------------------------------------------------ */
 static const double kDelta = 1e-8;   /* exclusion threshold of the relative errors (A13) */
 
+/* per-channel-asym ("quantize KV cache along the channel or token dimension"; Table
+ * tab:kvcache_quantization_error_per_channel_per_token_asym): every channel column of the whole trace
+ * [0, S) is one Eq. 2 group (O1 with stride d), for keys and values alike (A28). */
+static void static_per_channel(int bits, int d, int S, const uint16_t* X, double* Xhat) {
+    uint8_t* codes = (uint8_t*)malloc((size_t)S + 1);
+    for (int c = 0; c < d; ++c) {
+        if (bits == 16) {
+            for (int t = 0; t < S; ++t) Xhat[(size_t)t * d + c] = kvto_bf16_to_f32(X[(size_t)t * d + c]);
+            continue;
+        }
+        uint32_t meta;
+        kvto_quantize_group(X + c, S, d, bits, codes, &meta);
+        for (int t = 0; t < S; ++t) Xhat[(size_t)t * d + c] = kvto_dequant_value(codes[t], meta);
+    }
+    free(codes);
+}
+
 int kvto_sensitivity(int mode, int G, int R, const uint16_t* Q, int H_q, int T_q, int q_pos0,
                      const uint16_t* K, const uint16_t* V, int H_kv, int S, int d, double scale,
                      const int32_t* pair_bits, int n_pairs, double* out) {
@@ -470,7 +487,10 @@ int kvto_sensitivity(int mode, int G, int R, const uint16_t* Q, int H_q, int T_q
     int rc = 0;
     for (int p = 0; p < n_pairs && rc == 0; ++p) {
         int kb = pair_bits[2 * p], vb = pair_bits[2 * p + 1];
-        if (kvto_slice_bytes(mode, kb, vb, G, R, d, cap, sz) != 0) { rc = -1; break; }
+        const int pc = mode == KVTO_MODE_PER_CHANNEL;
+        if (pc ? (kb != 2 && kb != 4 && kb != 8 && kb != 16) || (vb != 2 && vb != 4 && vb != 8 && vb != 16)
+               : kvto_slice_bytes(mode, kb, vb, G, R, d, cap, sz) != 0) { rc = -1; break; }
+        if (pc) for (int i = 0; i < 6; ++i) sz[i] = 0;
         uint8_t* kc = (uint8_t*)malloc(sz[0] + 1); uint32_t* km = (uint32_t*)malloc(sz[1] + 4);
         uint16_t* kr = (uint16_t*)malloc(sz[2] + 2); uint8_t* vc = (uint8_t*)malloc(sz[3] + 1);
         uint32_t* vm = (uint32_t*)malloc(sz[4] + 4); uint16_t* vr = (uint16_t*)malloc(sz[5] + 2);
@@ -480,8 +500,13 @@ int kvto_sensitivity(int mode, int G, int R, const uint16_t* Q, int H_q, int T_q
             const uint16_t* Kx = K + (size_t)hk * nKV;
             const uint16_t* Vx = V + (size_t)hk * nKV;
             /* step 1: static O2 over the whole trace (A15), then read back K_hat, V_hat */
-            kvto_build_cache(mode, kb, vb, G, R, d, cap, S, Kx, Vx, kc, km, kr, vc, vm, vr);
-            kvto_dequant_cache(mode, kb, vb, G, R, d, cap, S, kc, km, kr, vc, vm, vr, Kh, Vh);
+            if (pc) {
+                static_per_channel(kb, d, S, Kx, Kh);
+                static_per_channel(vb, d, S, Vx, Vh);
+            } else {
+                kvto_build_cache(mode, kb, vb, G, R, d, cap, S, Kx, Vx, kc, km, kr, vc, vm, vr);
+                kvto_dequant_cache(mode, kb, vb, G, R, d, cap, S, kc, km, kr, vc, vm, vr, Kh, Vh);
+            }
             for (size_t i = 0; i < nKV; ++i) { Kf[i] = kvto_bf16_to_f32(Kx[i]); Vf[i] = kvto_bf16_to_f32(Vx[i]); }
             /* e_k, e_v = mean |X - X_hat| / |X| over |X| >= delta (A13) */
             for (size_t i = 0; i < nKV; ++i) {

@@ -21,7 +21,8 @@
 extern "C" {
 #endif
 
-enum { KVTO_MODE_PER_TOKEN = 0, KVTO_MODE_KIVI = 1 };
+enum { KVTO_MODE_PER_TOKEN = 0, KVTO_MODE_KIVI = 1,
+       KVTO_MODE_PER_CHANNEL = 2 /* sensitivity only: whole-sequence per-channel K and V (A28) */ };
 
 /* ---- bf16 helpers (the bf16 format: top 16 bits of an IEEE binary32) ---- */
 float    kvto_bf16_to_f32(uint16_t b);

@@ -243,7 +243,15 @@ extern "C" int32_t kvt_layer_sensitivity(int32_t mode, int32_t G, int32_t R, con
     if (S <= 0 || T_q <= 0 || q_pos0 < 0 || (int64_t)q_pos0 + T_q > S)
         return fail(KVT_ERR_INVALID_ARG, "sensitivity: need 0 <= q_pos0 and q_pos0 + T_q <= S");
     if (n_pairs <= 0) return fail(KVT_ERR_INVALID_ARG, "sensitivity: n_pairs must be > 0");
-    for (int i = 0; i < n_pairs; ++i) {
+    if (mode == KVT_MODE_PER_CHANNEL_ASYM) {   // whole-sequence statistics, no residual, no grouping (A28)
+        if (d != 128) return fail(KVT_ERR_UNSUPPORTED, "sensitivity: head_dim %d (128 only)", d);
+        if (R != 0) return fail(KVT_ERR_INVALID_ARG, "sensitivity: per-channel-asym has no residual (R = %d)", R);
+        for (int i = 0; i < n_pairs; ++i)
+            for (int b : {pairs[i].key_bits, pairs[i].value_bits})
+                if (b != 2 && b != 4 && b != 8 && b != 16)
+                    return fail(KVT_ERR_INVALID_ARG, "sensitivity: pair %d has %d bits", i, b);
+    }
+    for (int i = 0; i < n_pairs && mode != KVT_MODE_PER_CHANNEL_ASYM; ++i) {
         kvt_layer_spec s{mode, pairs[i].key_bits, pairs[i].value_bits, G, R};
         Geometry g;
         int cap = ((S + G - 1) / (G > 0 ? G : 1)) * G;

@@ -85,6 +85,33 @@ __global__ void __launch_bounds__(128) dequant_blocks_kernel(const uint16_t* __r
     }
 }
 
+// per-channel-asym (A28): every channel column of the whole trace is one Eq. 2 group, keys and values alike.
+// Block = one KV head: thread (slice, c) scans tokens slice, slice + 8, ... of channel c; the 8 slices'
+// min / max meet in shared memory (min / max are exact, so the order does not matter).
+__global__ void __launch_bounds__(1024) dequant_cols_kernel(const uint16_t* __restrict__ x, double* __restrict__ xh,
+                                                            int S, int bits) {
+    __shared__ float smn[8][D], smx[8][D];
+    const int h = blockIdx.x, c = threadIdx.x & (D - 1), sl = threadIdx.x >> 7;
+    const uint16_t* xc = x + (size_t)h * S * D + c;
+    float mn = INFINITY, mx = -INFINITY;
+    for (int t = sl; t < S; t += 8) {
+        const float f = bf2f(xc[(size_t)t * D]);
+        mn = fminf(mn, f);
+        mx = fmaxf(mx, f);
+    }
+    smn[sl][c] = mn;
+    smx[sl][c] = mx;
+    __syncthreads();
+    for (int j = 0; j < 8; ++j) { mn = fminf(mn, smn[j][c]); mx = fmaxf(mx, smx[j][c]); }
+    double* oc = xh + (size_t)h * S * D + c;
+    if (bits == 16) {
+        for (int t = sl; t < S; t += 8) oc[(size_t)t * D] = (double)bf2f(xc[(size_t)t * D]);
+        return;
+    }
+    const GroupQ q = group_params(mn, mx, bits);
+    for (int t = sl; t < S; t += 8) oc[(size_t)t * D] = dq(code_of(bf2f(xc[(size_t)t * D]), q), q.s_bits, q.z_bits);
+}
+
 // Block-level fp64 sum (fixed order).
 template <int NT>
 __device__ double block_sum(double v, double* red) {
@@ -265,14 +292,17 @@ int32_t launch_sensitivity(int mode, int G, int R, const uint16_t* q, int H_q, i
         const int kb = pairs[p].key_bits, vb = pairs[p].value_bits;
         const int nqK = nq_key(mode, kb, G, R, S);
         const int nqV = nq_per_token(vb, R, S);
-        if (mode == KVT_MODE_KIVI && kb != 16) {
+        if (mode == KVT_MODE_PER_CHANNEL_ASYM) {
+            dequant_cols_kernel<<<H_kv, 1024, 0, st>>>(k, Kh, S, kb);
+            dequant_cols_kernel<<<H_kv, 1024, 0, st>>>(v, Vh, S, vb);
+        } else if (mode == KVT_MODE_KIVI && kb != 16) {
             const int nblk = nqK / G;
             if (nblk > 0) dequant_blocks_kernel<<<dim3(H_kv, (nblk + 3) / 4), 128, 0, st>>>(k, Kh, S, kb, G, nqK);
             dequant_rows_kernel<<<rows_grid, 128, 0, st>>>(k, Kh, S, 16, G, S, nqK);   // exact residual rows
         } else {
             dequant_rows_kernel<<<rows_grid, 128, 0, st>>>(k, Kh, S, kb, G, nqK, 0);
         }
-        dequant_rows_kernel<<<rows_grid, 128, 0, st>>>(v, Vh, S, vb, G, nqV, 0);
+        if (mode != KVT_MODE_PER_CHANNEL_ASYM) dequant_rows_kernel<<<rows_grid, 128, 0, st>>>(v, Vh, S, vb, G, nqV, 0);
         relerr_kernel<<<kRedBlocks, 256, 0, st>>>(k, Kh, nel, pk);
         relerr_kernel<<<kRedBlocks, 256, 0, st>>>(v, Vh, nel, pv);
         attn_kernel<<<attn_grid, 128, attn_smem, st>>>(q, Kh, Vh, H_q, T_q, q_pos0, H_kv, S, sc, 1, aref, oref, err);

@@ -22,6 +22,7 @@ _LIB_PATH = Path(__file__).resolve().parent / os.environ.get("KVT_LIB", "libkvt.
 
 MODE_PER_TOKEN_ASYM = 0
 MODE_KIVI = 1
+MODE_PER_CHANNEL_ASYM = 2      # kvt_layer_sensitivity only (A28)
 _MODE_NAMES = {"per-token-asym": MODE_PER_TOKEN_ASYM, "kivi": MODE_KIVI}
 
 
