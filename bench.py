@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--workload", default="llama-3.25", choices=sorted(WORKLOADS))
     ap.add_argument("--batch", type=int, default=None, help="sequences per GPU (weak scaling)")
     ap.add_argument("--ctx", type=int, default=None, help="tokens in the cache after the first append")
+    ap.add_argument("--paged", action="store_true",
+                    help="paged tile records: every 32-token block in a shuffled page of a per-layer pool")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks / e2e / cpu baseline)")
@@ -265,7 +267,12 @@ def run_kvt(args):
     len0 = torch.zeros(B, dtype=torch.int32, device=dev)
     nS0 = torch.full((B,), S0, dtype=torch.int32, device=dev)
     for l, spec in enumerate(specs):
-        cache = kvt.LayerCache(spec, B, H, D, cap, device=dev)
+        if args.paged:        # vLLM-style: one block table per layer, pages assigned in a random order
+            pg = torch.Generator().manual_seed(500 + l)
+            bt = torch.randperm(B * (cap // 32), generator=pg).view(B, cap // 32).to(torch.int32).to(dev)
+            cache = kvt.LayerCache(spec, B, H, D, cap, device=dev, block_table=bt, num_pages=B * (cap // 32))
+        else:
+            cache = kvt.LayerCache(spec, B, H, D, cap, device=dev)
         gen.manual_seed(1000 * rank + l)
         Kp = torch.randn(B, H, S0, D, device=dev, generator=gen)
         Kp[..., ::8] *= 11.0                                  # kvt_synth recipe: key channel outliers
@@ -419,7 +426,8 @@ def run_kvt(args):
                            "batch_per_gpu": B, "ctx": f"{S_first}..{S_first + args.steps - 1}",
                            "parallelism": (f"sequence-sharded x{world} (partial -> NCCL all-gather -> combine)" if seqshard
                                            else f"batch-partitioned x{world} (no collective)"),
-                           "l2": "inputs larger than L2 (cache %.1f GB/GPU)" % (sum(c.nbytes for c in caches) / 1e9)},
+                           "l2": "inputs larger than L2 (cache %.1f GB/GPU)" % (sum(c.nbytes for c in caches) / 1e9),
+                           "kv_layout": "paged (shuffled 32-token pages, block table)" if args.paged else "dense"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": args.steps * ((1 if appends else 0) * L + L + (L if seqshard else 0) + n_combine),
                 "clocks": clocks,

@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define KVT_ABI_VERSION 1u
+#define KVT_ABI_VERSION 2u
 
 typedef enum {
     KVT_OK = 0,
@@ -112,7 +112,21 @@ typedef struct {
     int32_t batch, kv_heads, head_dim, capacity;
     void* k_codes; void* k_meta; void* k_resid;
     void* v_codes; void* v_meta; void* v_resid;
+    /* PAGED tile records (vLLM-style block table, "vLLM" P:85).  NULL = dense.
+     * Only for tile-record layers (else KVT_ERR_UNSUPPORTED).  Then k_codes is a pool of `num_pages`
+     * pages; page p holds the kv_heads records of one 32-token block: record (p, h) at
+     * k_codes + (p * kv_heads + h) * rec (rec as above; page bytes from kvt_page_bytes).  block_table:
+     * DEVICE int32 [batch][max_pages]; block j (tokens 32j .. 32j+31) of sequence b is page
+     * block_table[b * max_pages + j].  capacity must equal 32 * max_pages.  The residual buffers stay
+     * dense.  The caller owns the table and keeps the pages of live blocks distinct and < num_pages
+     * (the kernels do not check the entries: an out-of-range page is undefined behaviour). */
+    const int32_t* block_table;
+    int32_t max_pages, num_pages;
 } kvt_layer_cache;
+
+/* Bytes of one page (kv_heads tile records) of a paged cache with this spec; KVT_ERR_UNSUPPORTED when
+ * the spec has no tile records. */
+int32_t kvt_page_bytes(const kvt_layer_spec* spec, int32_t kv_heads, int32_t head_dim, uint64_t* bytes);
 
 /* Byte sizes of the six buffers for the whole layer, in the order of kvt_layer_cache
  * (k_codes, k_meta, k_resid, v_codes, v_meta, v_resid); 0 for an absent buffer. */

@@ -71,6 +71,16 @@ static int32_t cache_geometry(const kvt_layer_cache* c, Geometry* g, CachePtrs* 
     if (!c) return fail(KVT_ERR_INVALID_ARG, "null cache");
     int32_t st = make_geometry(c->spec, c->batch, c->kv_heads, c->head_dim, c->capacity, g);
     if (st) return st;
+    p->bt = c->block_table;
+    p->max_pages = 0;
+    if (c->block_table) {
+        if (!g->v_blocked) return fail(KVT_ERR_UNSUPPORTED, "paged caches need tile records (G = 32, d = 128, 2/4/8-bit K and V)");
+        if (c->max_pages <= 0 || c->num_pages <= 0 || (int64_t)c->max_pages * 32 != c->capacity)
+            return fail(KVT_ERR_INVALID_ARG, "paged cache: max_pages %d, num_pages %d, capacity %d (must be 32 * max_pages)",
+                        c->max_pages, c->num_pages, c->capacity);
+        if ((uintptr_t)c->block_table & 3) return fail(KVT_ERR_INVALID_ARG, "block_table must be 4-byte aligned");
+        p->max_pages = c->max_pages;
+    }
     const char* names[6] = {"k_codes", "k_meta", "k_resid", "v_codes", "v_meta", "v_resid"};
     void* ptrs[6] = {c->k_codes, c->k_meta, c->k_resid, c->v_codes, c->v_meta, c->v_resid};
     size_t sz[6] = {g->kc, g->km, g->kr, g->vc, g->vm, g->vr};
@@ -122,6 +132,17 @@ extern "C" int32_t kvt_cache_buffer_sizes(const kvt_layer_spec* spec, int32_t ba
     uint64_t n = (uint64_t)batch * (uint64_t)kv_heads;
     out[0] = n * g.kc; out[1] = n * g.km; out[2] = n * g.kr;
     out[3] = n * g.vc; out[4] = n * g.vm; out[5] = n * g.vr;
+    return KVT_OK;
+}
+
+extern "C" int32_t kvt_page_bytes(const kvt_layer_spec* spec, int32_t kv_heads, int32_t head_dim, uint64_t* bytes) {
+    clear_error();
+    if (!spec || !bytes) return fail(KVT_ERR_INVALID_ARG, "null argument");
+    Geometry g;
+    int32_t st = make_geometry(*spec, 1, kv_heads, head_dim, 32, &g);
+    if (st) return st;
+    if (!g.v_blocked) return fail(KVT_ERR_UNSUPPORTED, "paged caches need tile records (G = 32, d = 128, 2/4/8-bit K and V)");
+    *bytes = (uint64_t)kv_heads * g.rec;
     return KVT_OK;
 }
 

@@ -200,13 +200,19 @@ __device__ __forceinline__ void bf16x4(const uint16_t* p, float x[4]) {
 struct Slice {
     const uint8_t* kc; const uint32_t* km; const uint16_t* kr;
     const uint8_t* vc; const uint32_t* vm; const uint16_t* vr;
+    const int32_t* bt = nullptr;   // paged tile records: this sequence's block-table row (kc = pool + h * rec)
+    size_t pstride = 0;            // page bytes (H records)
+    // tile record j of this (b, h) slice
+    __device__ __forceinline__ const uint8_t* recp(int j, const Geometry& g) const {
+        return bt ? kc + (size_t)bt[j] * pstride : kc + (size_t)j * g.rec;
+    }
 };
 
 // REC: tile records (g.rec) — token t's key row and block meta live in record t / 32.
 template <int KB, bool KPC, bool REC = false>
 __device__ __forceinline__ void tail_k(const Slice& s, const Geometry& g, int t, int nqK, int lane, float x[4]) {
     if (t < nqK) {
-        const uint8_t* row = REC ? s.kc + (size_t)(t >> 5) * g.rec + (size_t)(t & 31) * g.row_k
+        const uint8_t* row = REC ? s.recp(t >> 5, g) + (size_t)(t & 31) * g.row_k
                                  : s.kc + (size_t)t * g.row_k;
         if constexpr (KB == 16) {
             bf16x4(reinterpret_cast<const uint16_t*>(row) + 4 * lane, x);
@@ -214,14 +220,14 @@ __device__ __forceinline__ void tail_k(const Slice& s, const Geometry& g, int t,
             uint32_t c[4];
             codes4<KB>(row, lane, c);
             if constexpr (KPC) {
-                const uint32_t* mb = REC ? reinterpret_cast<const uint32_t*>(s.kc + (size_t)(t >> 5) * g.rec + g.rec_km)
+                const uint32_t* mb = REC ? reinterpret_cast<const uint32_t*>(s.recp(t >> 5, g) + g.rec_km)
                                          : s.km + (size_t)(t / g.G) * D;
                 uint4 m = reinterpret_cast<const uint4*>(mb)[lane];
                 uint32_t mm[4] = {m.x, m.y, m.z, m.w};
 #pragma unroll
                 for (int i = 0; i < 4; ++i) x[i] = fmaf((float)c[i], bf2f(mm[i] & 0xffffu), bf2f(mm[i] >> 16));
             } else {
-                const uint32_t* mr = REC ? reinterpret_cast<const uint32_t*>(s.kc + (size_t)(t >> 5) * g.rec + g.rec_km +
+                const uint32_t* mr = REC ? reinterpret_cast<const uint32_t*>(s.recp(t >> 5, g) + g.rec_km +
                                                                              (size_t)(t & 31) * 16)
                                          : s.km + (size_t)t * (D / g.G);
                 uint32_t m = mr[(4 * lane) / g.G];
@@ -260,7 +266,7 @@ __device__ __forceinline__ void tail_v(const Slice& s, const Geometry& g, int t,
     if (t < nqV) {
         const uint8_t* row = s.vc + (size_t)t * g.row_v;
         if constexpr (REC && VB != 16) {
-            const uint8_t* rec = s.kc + (size_t)(t >> 5) * g.rec;
+            const uint8_t* rec = s.recp(t >> 5, g);
             uint32_t c[4];
             codes4_blk<VB>(rec + g.rec_vc, t, lane, c);
             const uint32_t m = reinterpret_cast<const uint32_t*>(rec + g.rec_vm + (size_t)(t & 31) * 16)[(4 * lane) / g.G];

@@ -311,7 +311,9 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
 
     const size_t bh = (size_t)b * g.H + hk;
     Slice sl;
-    sl.kc = a.c.k_codes + bh * g.kc;
+    // paged: kc = the pool base of head hk and record j is page bt[b][j] (read from the kernel parameters
+    // where used, so the main loop keeps no extra registers)
+    sl.kc = a.c.bt ? a.c.k_codes + (size_t)hk * g.rec : a.c.k_codes + bh * g.kc;
     sl.km = nullptr;                                 // tile records: K meta, V codes and V meta live in kc
     sl.kr = a.c.k_resid + bh * (g.kr / 2);
     sl.vc = nullptr;
@@ -325,6 +327,10 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
     // ---- stage the tail rows [n_main, S) into shared memory with bulk copies (one round trip instead of a
     // dependent global load per token group); `tl` then addresses them with the cache's own indexing ----
     Slice tl = sl;
+    if (a.c.bt) {
+        tl.bt = a.c.bt + (size_t)b * a.c.max_pages;
+        tl.pstride = (size_t)g.H * g.rec;
+    }
     uint64_t* tbar = reinterpret_cast<uint64_t*>(smem + Gm::Q_BYTES + Gm::TAIL_PART);
     bool staged = false;
     if (KVT_EXP != 5 && do_tail && n_main < S) {
@@ -346,12 +352,19 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
                 asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
                 fence_proxy_async();
                 mbar_expect_tx(tbar, total);
-                if (b_rec) bulk_g2s(p_rec, sl.kc + (size_t)r0 * Gm::STAGE, b_rec, tbar);
+                if (b_rec) {
+                    if (tl.bt) {
+                        for (int r = r0; r < r1; ++r) bulk_g2s(p_rec + (size_t)(r - r0) * Gm::STAGE, tl.recp(r, g), Gm::STAGE, tbar);
+                    } else {
+                        bulk_g2s(p_rec, sl.kc + (size_t)r0 * Gm::STAGE, b_rec, tbar);
+                    }
+                }
                 if (b_kr) bulk_g2s(p_kr, sl.kr, b_kr, tbar);
                 if (b_vr) bulk_g2s(p_vr, sl.vr, b_vr, tbar);
             }
             // virtual bases: record r of the cache lands at its staged copy under the cache's own indexing
             tl.kc = p_rec - (size_t)r0 * Gm::STAGE;
+            tl.bt = nullptr;
             tl.kr = reinterpret_cast<const uint16_t*>(p_kr);
             tl.vr = reinterpret_cast<const uint16_t*>(p_vr);
         }
@@ -560,7 +573,9 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
         const int t0 = (tile_lo + warp + it * kWarps) * kTile;
         uint8_t* sb = wbase + st * Gm::STAGE;
         mbar_expect_tx(bars + st, Gm::STAGE);
-        bulk_g2s(sb, sl.kc + (size_t)(t0 / kTile) * Gm::STAGE, Gm::STAGE, bars + st);   // one tile record
+        const uint8_t* src = a.c.bt ? a.c.k_codes + ((size_t)a.c.bt[(size_t)b * a.c.max_pages + t0 / kTile] * g.H + hk) * Gm::STAGE
+                                    : sl.kc + (size_t)(t0 / kTile) * Gm::STAGE;
+        bulk_g2s(sb, src, Gm::STAGE, bars + st);     // one tile record
     };
 
     // generic-proxy writes to the ring area (tail scratch) are ordered before the first bulk copies; later

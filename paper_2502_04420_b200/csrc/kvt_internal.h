@@ -68,6 +68,8 @@ int32_t make_geometry(const kvt_layer_spec& s, int B, int H, int d, int cap, Geo
 struct CachePtrs {
     uint8_t* k_codes; uint32_t* k_meta; uint16_t* k_resid;
     uint8_t* v_codes; uint32_t* v_meta; uint16_t* v_resid;
+    const int32_t* bt;     // paged tile records: block table [B][max_pages] (device), or null (dense)
+    int max_pages;
 };
 int32_t launch_append(const Geometry& g, const CachePtrs& c, const uint16_t* k_new, const uint16_t* v_new,
                       const int64_t strides[3], const int32_t* len_before, const int32_t* n_new,

@@ -78,16 +78,20 @@ __device__ void quant_block_warp(Src src, int G, int bits, uint8_t* codes0, size
 // Token t's packed row and meta row; with tile records (g.rec) they live in the record of block t / 32
 // (codes = the record base; the row pointer is unused: the codes go to the blocked V block).
 // With tile records: rows at blk_off == 0 are token-major code rows (K), otherwise the blocked V block.
+// Paged caches (bt != null): record j of the sequence is page bt[j]; codes = the pool base of this KV head
+// and pstride = the page size (H records).
 struct TokDst {
     uint8_t* codes; uint32_t* meta; size_t row_bytes; int gpr; size_t rec; uint32_t blk_off, meta_off;
+    const int32_t* bt; size_t pstride;
+    __device__ uint8_t* recp(int j) const { return bt ? codes + (size_t)bt[j] * pstride : codes + (size_t)j * rec; }
     __device__ uint8_t* row(int t) const {
-        return rec ? codes + (size_t)(t >> 5) * rec + (size_t)(t & 31) * row_bytes : codes + (size_t)t * row_bytes;
+        return rec ? recp(t >> 5) + (size_t)(t & 31) * row_bytes : codes + (size_t)t * row_bytes;
     }
     __device__ uint32_t* meta_row(int t) const {
-        return rec ? reinterpret_cast<uint32_t*>(codes + (size_t)(t >> 5) * rec + meta_off + (size_t)(t & 31) * 16)
+        return rec ? reinterpret_cast<uint32_t*>(recp(t >> 5) + meta_off + (size_t)(t & 31) * 16)
                    : meta + (size_t)t * gpr;
     }
-    __device__ uint8_t* vblk(int t) const { return rec && blk_off ? codes + (size_t)(t >> 5) * rec + blk_off : nullptr; }
+    __device__ uint8_t* vblk(int t) const { return rec && blk_off ? recp(t >> 5) + blk_off : nullptr; }
 };
 
 __device__ void per_token_tensor(int phase, int bits, int G, int R, int L0, int S, const uint16_t* in,
@@ -161,7 +165,8 @@ __device__ void per_token_tensor(int phase, int bits, int G, int R, int L0, int 
 // append and t - na after it.
 __device__ void per_channel_key(int phase, int bits, int G, int F, int L0, int S, const uint16_t* in, int64_t s2,
                                 uint8_t* codes, size_t row_bytes, uint32_t* meta, uint16_t* resid, int wid,
-                                int nwarps, int lane, size_t rec = 0, uint32_t rec_km = 0) {
+                                int nwarps, int lane, size_t rec = 0, uint32_t rec_km = 0,
+                                const int32_t* bt = nullptr, size_t pstride = 0) {
     int nb = F * (L0 / F);
     int na = F * (S / F);
     int nblk = (na - nb) / G;
@@ -170,9 +175,9 @@ __device__ void per_channel_key(int phase, int bits, int G, int F, int L0, int S
             int t0 = nb + j * G;
             bool from_resid = t0 < L0;
             if ((phase == 0) != from_resid) continue;
-            uint8_t* cblk = rec ? codes + (size_t)(t0 / G) * rec : codes + (size_t)t0 * row_bytes;
-            uint32_t* mblk = rec ? reinterpret_cast<uint32_t*>(codes + (size_t)(t0 / G) * rec + rec_km)
-                                 : meta + (size_t)(t0 / G) * 128;
+            uint8_t* rp = bt ? codes + (size_t)bt[t0 / G] * pstride : codes + (size_t)(t0 / G) * rec;
+            uint8_t* cblk = rec ? rp : codes + (size_t)t0 * row_bytes;
+            uint32_t* mblk = rec ? reinterpret_cast<uint32_t*>(rp + rec_km) : meta + (size_t)(t0 / G) * 128;
             if (from_resid) {
                 auto src = [&](int i) -> const uint2* {
                     int t = t0 + i;
@@ -204,7 +209,9 @@ __global__ void __launch_bounds__(kWarps * 32) append_kernel(AppendArgs a) {
     const int S = L0 + n;
     const Geometry& g = a.g;
     const size_t bh = (size_t)b * g.H + h;
-    uint8_t* kc = a.c.k_codes + bh * g.kc;
+    const int32_t* bt = a.c.bt ? a.c.bt + (size_t)b * a.c.max_pages : nullptr;    // paged (tile records only)
+    const size_t pstride = (size_t)g.H * g.rec;
+    uint8_t* kc = bt ? a.c.k_codes + (size_t)h * g.rec : a.c.k_codes + bh * g.kc;
     uint32_t* km = g.km ? a.c.k_meta + bh * (g.km / 4) : nullptr;
     uint16_t* kr = g.kr ? a.c.k_resid + bh * (g.kr / 2) : nullptr;
     uint8_t* vc = a.c.v_codes + bh * g.vc;
@@ -212,22 +219,22 @@ __global__ void __launch_bounds__(kWarps * 32) append_kernel(AppendArgs a) {
     uint16_t* vr = g.vr ? a.c.v_resid + bh * (g.vr / 2) : nullptr;
     const uint16_t* kin = a.k_new + (int64_t)b * a.s0 + (int64_t)h * a.s1;
     const uint16_t* vin = a.v_new + (int64_t)b * a.s0 + (int64_t)h * a.s1;
-    const TokDst kd = g.rec ? TokDst{kc, nullptr, g.row_k, 128 / g.G, g.rec, 0, g.rec_km}   // per-token K rows in records
-                            : TokDst{kc, km, g.row_k, 128 / g.G, 0, 0, 0};
-    const TokDst vd = g.rec ? TokDst{kc, nullptr, g.row_v, 128 / g.G, g.rec, g.rec_vc, g.rec_vm}
-                            : TokDst{vc, vm, g.row_v, 128 / g.G, 0, 0, 0};
+    const TokDst kd = g.rec ? TokDst{kc, nullptr, g.row_k, 128 / g.G, g.rec, 0, g.rec_km, bt, pstride}   // per-token K rows in records
+                            : TokDst{kc, km, g.row_k, 128 / g.G, 0, 0, 0, nullptr, 0};
+    const TokDst vd = g.rec ? TokDst{kc, nullptr, g.row_v, 128 / g.G, g.rec, g.rec_vc, g.rec_vm, bt, pstride}
+                            : TokDst{vc, vm, g.row_v, 128 / g.G, 0, 0, 0, nullptr, 0};
 
     // phase 0 (chunk 0): residual-sourced groups; phase 1: input-sourced groups (everyone)
     if (chunk == 0) {
         if (g.key_per_channel)
-            per_channel_key(0, g.kb, g.G, g.F, L0, S, kin, a.s2, kc, g.row_k, km, kr, warp, kWarps, lane, g.rec, g.rec_km);
+            per_channel_key(0, g.kb, g.G, g.F, L0, S, kin, a.s2, kc, g.row_k, km, kr, warp, kWarps, lane, g.rec, g.rec_km, bt, pstride);
         else
             per_token_tensor(0, g.kb, g.G, g.R, L0, S, kin, a.s2, kd, kr, warp, kWarps, lane);
         per_token_tensor(0, g.vb, g.G, g.R, L0, S, vin, a.s2, vd, vr, warp, kWarps, lane);
     }
     const int wid = chunk * kWarps + warp, nw = gridDim.x * kWarps;
     if (g.key_per_channel)
-        per_channel_key(1, g.kb, g.G, g.F, L0, S, kin, a.s2, kc, g.row_k, km, kr, wid, nw, lane, g.rec, g.rec_km);
+        per_channel_key(1, g.kb, g.G, g.F, L0, S, kin, a.s2, kc, g.row_k, km, kr, wid, nw, lane, g.rec, g.rec_km, bt, pstride);
     else
         per_token_tensor(1, g.kb, g.G, g.R, L0, S, kin, a.s2, kd, kr, wid, nw, lane);
     per_token_tensor(1, g.vb, g.G, g.R, L0, S, vin, a.s2, vd, vr, wid, nw, lane);
@@ -235,7 +242,7 @@ __global__ void __launch_bounds__(kWarps * 32) append_kernel(AppendArgs a) {
     if (chunk == 0) {
         __syncthreads();
         if (g.key_per_channel)
-            per_channel_key(2, g.kb, g.G, g.F, L0, S, kin, a.s2, kc, g.row_k, km, kr, warp, kWarps, lane, g.rec, g.rec_km);
+            per_channel_key(2, g.kb, g.G, g.F, L0, S, kin, a.s2, kc, g.row_k, km, kr, warp, kWarps, lane, g.rec, g.rec_km, bt, pstride);
         else
             per_token_tensor(2, g.kb, g.G, g.R, L0, S, kin, a.s2, kd, kr, warp, kWarps, lane);
         per_token_tensor(2, g.vb, g.G, g.R, L0, S, vin, a.s2, vd, vr, warp, kWarps, lane);

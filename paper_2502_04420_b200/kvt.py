@@ -41,7 +41,8 @@ class _Cache(ctypes.Structure):
     _fields_ = [("spec", _Spec), ("batch", ctypes.c_int32), ("kv_heads", ctypes.c_int32),
                 ("head_dim", ctypes.c_int32), ("capacity", ctypes.c_int32),
                 ("k_codes", ctypes.c_void_p), ("k_meta", ctypes.c_void_p), ("k_resid", ctypes.c_void_p),
-                ("v_codes", ctypes.c_void_p), ("v_meta", ctypes.c_void_p), ("v_resid", ctypes.c_void_p)]
+                ("v_codes", ctypes.c_void_p), ("v_meta", ctypes.c_void_p), ("v_resid", ctypes.c_void_p),
+                ("block_table", ctypes.c_void_p), ("max_pages", ctypes.c_int32), ("num_pages", ctypes.c_int32)]
 
 
 class _Pair(ctypes.Structure):
@@ -77,6 +78,7 @@ def _load():
         "kvt_sensitivity_workspace_bytes": (i32, [i32, i32, i32, i32, i32, i32, ctypes.POINTER(u64)]),
         "kvt_layer_sensitivity": (i32, [i32, i32, i32, P, i32, i32, i32, P, P, i32, i32, i32, ctypes.c_float,
                                         ctypes.POINTER(_Pair), i32, P, P, u64, P]),
+        "kvt_page_bytes": (i32, [ctypes.POINTER(_Spec), i32, i32, ctypes.POINTER(u64)]),
         "kvt_pareto_prune": (i32, [ctypes.POINTER(_Pair), P, i32, P]),
         "kvt_dbscan": (i32, [P, i32, i32, ctypes.c_double, i32, P]),
         "kvt_prune_and_cluster": (i32, [ctypes.POINTER(_Pair), i32, P, i32, ctypes.c_double, i32, P, P,
@@ -97,7 +99,7 @@ EXPORTED = ("kvt_abi_version", "kvt_status_string", "kvt_last_error", "kvt_confi
             "kvt_config_free", "kvt_validate_spec", "kvt_cache_buffer_sizes", "kvt_quantize_append",
             "kvt_decode_workspace_bytes", "kvt_decode_attention", "kvt_decode_attention_partial",
             "kvt_combine_partials", "kvt_sensitivity_workspace_bytes", "kvt_layer_sensitivity",
-            "kvt_pareto_prune", "kvt_dbscan", "kvt_prune_and_cluster", "kvt_search_space_log10")
+            "kvt_pareto_prune", "kvt_dbscan", "kvt_prune_and_cluster", "kvt_search_space_log10", "kvt_page_bytes")
 
 
 def lib():
@@ -200,18 +202,43 @@ def cache_buffer_sizes(spec: LayerSpec, batch: int, kv_heads: int, head_dim: int
 BUFFER_NAMES = ("k_codes", "k_meta", "k_resid", "v_codes", "v_meta", "v_resid")
 
 
+def page_bytes(spec: "LayerSpec", kv_heads: int, head_dim: int = 128) -> int:
+    """Bytes of one page (kv_heads tile records of 32 tokens) of a paged cache (include/kvt.h)."""
+    out = ctypes.c_uint64()
+    _check(_lib.kvt_page_bytes(ctypes.byref(spec._c()), kv_heads, head_dim, ctypes.byref(out)))
+    return int(out.value)
+
+
 class LayerCache:
-    """One layer's packed cache; the six buffers are torch uint8 tensors owned here."""
+    """One layer's packed cache; the six buffers are torch uint8 tensors owned here.
+
+    Paged (vLLM-style) when `block_table` is given: an int32 [batch][max_pages] device tensor mapping
+    32-token block j of sequence b to a page of a pool of `num_pages` pages (k_codes); capacity is then
+    32 * max_pages.  The caller owns the table and its allocation policy."""
 
     def __init__(self, spec: LayerSpec, batch: int, kv_heads: int, head_dim: int, capacity: int,
-                 device="cuda"):
+                 device="cuda", block_table: Optional[torch.Tensor] = None, num_pages: Optional[int] = None):
         self.spec, self.batch, self.kv_heads, self.head_dim, self.capacity = spec, batch, kv_heads, head_dim, capacity
         sizes = cache_buffer_sizes(spec, batch, kv_heads, head_dim, capacity)
+        self.block_table = block_table
+        if block_table is not None:
+            _dev(block_table, "block_table", torch.int32)
+            if block_table.dim() != 2 or block_table.shape[0] != batch or not block_table.is_contiguous():
+                raise ValueError("block_table must be a contiguous int32 [batch][max_pages] tensor")
+            if capacity != 32 * block_table.shape[1]:
+                raise ValueError("paged cache: capacity must be 32 * max_pages")
+            if not num_pages or num_pages < 1:
+                raise ValueError("paged cache: num_pages >= 1 required")
+            sizes = list(sizes)
+            sizes[0] = num_pages * page_bytes(spec, kv_heads, head_dim)
+        self.num_pages = num_pages if block_table is not None else 0
         self.sizes = dict(zip(BUFFER_NAMES, sizes))
         self.buffers = {n: (torch.empty(max(sz, 16), dtype=torch.uint8, device=device) if sz else None)
                         for n, sz in self.sizes.items()}
         self._c = _Cache(spec._c(), batch, kv_heads, head_dim, capacity,
-                         *[(b.data_ptr() if b is not None else None) for b in self.buffers.values()])
+                         *[(b.data_ptr() if b is not None else None) for b in self.buffers.values()],
+                         block_table.data_ptr() if block_table is not None else None,
+                         block_table.shape[1] if block_table is not None else 0, self.num_pages)
 
     def slice_view(self, name: str, b: int, h: int) -> torch.Tensor:
         """Bytes of buffer `name` for (batch row b, kv head h)."""

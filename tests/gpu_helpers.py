@@ -37,7 +37,8 @@ def compare_slice(oracle, cache, spec, b, h, K_bits, V_bits, S, d=128):
     for name, (exp, mask) in ref.items():
         if cache.buffers[name] is None or not mask.any():
             continue
-        gpu = cache.slice_view(name, b, h).cpu().numpy().view(np.uint8)
+        gpu = (paged_records(cache, b, h) if name == "k_codes" and getattr(cache, "block_table", None) is not None
+               else cache.slice_view(name, b, h)).cpu().numpy().view(np.uint8)
         bad = np.nonzero((gpu != exp) & mask)[0]
         if bad.size:
             raise AssertionError(f"{name} (b={b}, h={h}, S={S}) differs at bytes {bad[:8]} "
@@ -52,6 +53,15 @@ def compare_slice(oracle, cache, spec, b, h, K_bits, V_bits, S, d=128):
         assert int(ref["k_codes"][1].sum()) == nqk * rk + kmeta + nqv * rv + nqv * 16
     else:
         assert int(ref["v_codes"][1].sum()) == nqv * rv
+
+
+def paged_records(cache, b, h):
+    """The tile records of (b, h) of a paged cache, gathered through its block table into the dense
+    order (record j = block j), i.e. the bytes a dense cache would hold."""
+    H, max_pages = cache.kv_heads, cache.block_table.shape[1]
+    rec = cache.sizes["k_codes"] // (cache.num_pages * H)
+    pool = cache.buffers["k_codes"][: cache.num_pages * H * rec].view(cache.num_pages, H, rec)
+    return pool[cache.block_table[b].long(), h].reshape(max_pages * rec)
 
 
 def rel_row_err(out, ref):

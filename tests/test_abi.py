@@ -28,7 +28,7 @@ def test_exports_every_declared_symbol(kvt):
     for name in sorted(declared):
         assert hasattr(lib, name), f"libkvt.so does not export {name}"
     assert set(kvt.kvt.EXPORTED) == declared
-    assert kvt.ABI_VERSION == 1
+    assert kvt.ABI_VERSION == 2          # 2: paged tile records (block_table fields of kvt_layer_cache)
 
 
 def test_status_strings(kvt):
@@ -130,3 +130,15 @@ def test_validation(kvt):
     assert e.value.status == 1
     kvt.validate_spec(kvt.LayerSpec.kivi(4, 2))
     kvt.validate_spec(kvt.LayerSpec.per_token(8, 4, group=128))
+
+
+def test_page_bytes():
+    """One page = kv_heads tile records of 32(16 b_k + 16 b_v) + 1024 bytes; no tile records
+    (bf16 keys, G = 64) -> unsupported."""
+    import paper_2502_04420_b200 as kvt
+
+    assert kvt.page_bytes(kvt.LayerSpec.kivi(4, 2), 8) == 8 * (32 * (16 * 4 + 16 * 2) + 1024)
+    assert kvt.page_bytes(kvt.LayerSpec.per_token(8, 8), 4) == 4 * (32 * 256 + 1024)
+    for spec in (kvt.LayerSpec.kivi(16, 4), kvt.LayerSpec.per_token(4, 4, group=64)):
+        with pytest.raises(kvt.KvtError):
+            kvt.page_bytes(spec, 8)
