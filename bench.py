@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--workload", default="llama-3.25", choices=sorted(WORKLOADS))
     ap.add_argument("--batch", type=int, default=None, help="sequences per GPU (weak scaling)")
     ap.add_argument("--ctx", type=int, default=None, help="tokens in the cache after the first append")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "symm"],
+                    help="seqshard workloads: NCCL all-gather of the partials, or the fused push into the peers' "
+                         "symmetric-memory buffers (kvt_decode_attention_partial_push + one barrier)")
     ap.add_argument("--paged", action="store_true",
                     help="paged tile records: every 32-token block in a shuffled page of a per-layer pool")
     ap.add_argument("--no-e2e", action="store_true")
@@ -307,9 +310,17 @@ def run_kvt(args):
     ones = torch.ones(B, dtype=torch.int32, device=dev)
     scale = 1.0 / math.sqrt(D)
     stream = torch.cuda.current_stream()
+    exch = None
     if seqshard:
         part = torch.empty(B, Hq, D + 2, dtype=torch.float32, device=dev)
         gathered = torch.empty(world, B, Hq, D + 2, dtype=torch.float32, device=dev)
+        if args.exchange == "symm":
+            from paper_2502_04420_b200.seqshard import SymmExchange
+
+            if world == 1 and not dist.is_initialized():
+                dist.init_process_group("nccl", init_method="tcp://127.0.0.1:29533", rank=0, world_size=1,
+                                        device_id=dev)
+            exch = SymmExchange((B, Hq, D + 2), dev)
 
     def step(ev=None, bs=0):
         q, k_new, v_new, outs = bufsets[bs]
@@ -318,7 +329,16 @@ def run_kvt(args):
                 kvt.quantize_append(caches[l], k_new[l], v_new[l], len_before, ones, n_new_max=1, stream=stream)
             if ev is not None:
                 ev[l][0].record(stream)
-            if seqshard:
+            if exch is not None:          # fused exchange: push into the peers' buffers, barrier, combine
+                k = exch.k
+                kvt.decode_attention_partial_push(caches[l], q[l], len_after, exch.slots[k], scale=scale,
+                                                  workspace=ws, stream=stream)
+                if ev is not None:
+                    ev[l][1].record(stream)
+                exch.handle.barrier(channel=0)
+                exch.k ^= 1
+                kvt.combine_partials(exch.buf[k], out=outs[l], stream=stream)
+            elif seqshard:
                 kvt.decode_attention_partial(caches[l], q[l], len_after, scale=scale, partial=part, workspace=ws,
                                              stream=stream)
                 if ev is not None:
@@ -457,7 +477,9 @@ def run_kvt(args):
                 "data": "synthetic (N(0,1) K with x11 outliers on channels c%8==0, N(0,1) V, 0.5 N(0,1) q)",
                 "config": {"workload": args.workload, "layers": desc, "shape": {"L": L, "H_kv": H, "H_q": Hq, "d": D},
                            "batch_per_gpu": B, "ctx": f"{S_first}..{S_first + args.steps - 1}",
-                           "parallelism": (f"sequence-sharded x{world} (partial -> NCCL all-gather -> combine)" if seqshard
+                           "parallelism": ((f"sequence-sharded x{world} (partial pushed into peer symmetric memory -> barrier -> combine)"
+                                            if exch is not None else
+                                            f"sequence-sharded x{world} (partial -> NCCL all-gather -> combine)") if seqshard
                                            else f"batch-partitioned x{world} (no collective)"),
                            "l2": "inputs larger than L2 (cache %.1f GB/GPU)" % (sum(c.nbytes for c in caches) / 1e9),
                            "kv_layout": "paged (shuffled 32-token pages, block table)" if args.paged else "dense"},

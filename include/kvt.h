@@ -175,6 +175,16 @@ int32_t kvt_decode_attention_partial(const kvt_layer_cache* cache, const void* q
                                      const int32_t* seq_len_host, const int32_t* seq_len_dev,
                                      float softmax_scale, float* partial,
                                      void* workspace, uint64_t ws_bytes, void* stream);
+/* a6 with the exchange fused into the attention kernel ("push"): as kvt_decode_attention_partial, but every
+ * (m, l, o) row is stored straight into each of the n_dst (1..8) destinations — typically this shard's slot
+ * of every rank's gathered buffer, mapped into this GPU's address space over NVLink (symmetric memory /
+ * CUDA IPC), so the all-gather happens in the kernel's epilogue and the ranks only need a barrier before
+ * kvt_combine_partials.  dsts: HOST array of device pointers, each to a [B][H_q][d + 2] fp32 block, 4-byte
+ * aligned.  Visibility to the peers is the caller's: a system-scope barrier after this call in stream order. */
+int32_t kvt_decode_attention_partial_push(const kvt_layer_cache* cache, const void* q, int32_t n_q_heads,
+                                          const int32_t* seq_len_host, const int32_t* seq_len_dev,
+                                          float softmax_scale, float* const* dsts, int32_t n_dst,
+                                          void* workspace, uint64_t ws_bytes, void* stream);
 int32_t kvt_combine_partials(const float* gathered, int32_t n_shards, int32_t batch,
                              int32_t n_q_heads, int32_t head_dim, void* out, int32_t out_dtype,
                              void* stream);

@@ -234,6 +234,22 @@ extern "C" int32_t kvt_decode_attention_partial(const kvt_layer_cache* cache, co
     return launch_decode(g, p, (const uint16_t*)q, H_q, seq_len_dev, plan, scale, partial, 2, ws, ws_bytes, stream);
 }
 
+extern "C" int32_t kvt_decode_attention_partial_push(const kvt_layer_cache* cache, const void* q, int32_t H_q,
+                                                     const int32_t* seq_len_host, const int32_t* seq_len_dev,
+                                                     float scale, float* const* dsts, int32_t n_dst, void* ws,
+                                                     uint64_t ws_bytes, void* stream) {
+    clear_error();
+    Geometry g; CachePtrs p; int plan;
+    int32_t st = decode_common(cache, q, H_q, seq_len_host, seq_len_dev, &g, &p, &plan);
+    if (st) return st;
+    if (!dsts || n_dst < 1 || n_dst > 8) return fail(KVT_ERR_INVALID_ARG, "decode push: need 1..8 destinations (got %d)", n_dst);
+    for (int i = 0; i < n_dst; ++i)
+        if (!dsts[i] || ((uintptr_t)dsts[i] & 3)) return fail(KVT_ERR_INVALID_ARG, "decode push: destination %d is null or misaligned", i);
+    if (g.B == 0) return KVT_OK;
+    return launch_decode(g, p, (const uint16_t*)q, H_q, seq_len_dev, plan, scale, dsts[0], 2, ws, ws_bytes, stream,
+                         dsts, n_dst);
+}
+
 extern "C" int32_t kvt_combine_partials(const float* gathered, int32_t n_shards, int32_t B, int32_t H_q,
                                         int32_t d, void* out, int32_t out_dtype, void* stream) {
     clear_error();

@@ -24,7 +24,7 @@ KFn get_decode_mma_k8(int VB, int GM, bool kpt, size_t* smem);
 // K3: merge n_parts partial rows [n_parts][rows][2 + D] -> out (bf16 / fp32 / partial).  One warp
 // per row; lane owns 4 channels.
 __global__ void __launch_bounds__(128) combine_kernel(const float* __restrict__ parts, int n_parts, int rows,
-                                                      void* out, int out_mode) {
+                                                      void* out, int out_mode, PushList push) {
     const int row = blockIdx.x * 4 + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (row >= rows) return;
@@ -43,10 +43,9 @@ __global__ void __launch_bounds__(128) combine_kernel(const float* __restrict__ 
         }
     }
     if (out_mode == 2) {
-        float* pr = reinterpret_cast<float*>(out) + (size_t)row * (2 + D);
-        if (lane == 0) { pr[0] = M; pr[1] = L; }
 #pragma unroll
-        for (int i = 0; i < 4; ++i) pr[2 + 4 * lane + i] = L > 0.0f ? __fdiv_rn(o[i], L) : 0.0f;
+        for (int i = 0; i < 4; ++i)
+            store_partial(push, out, (size_t)row, 4 * lane + i, M, L, L > 0.0f ? __fdiv_rn(o[i], L) : 0.0f);
         return;
     }
 #pragma unroll
@@ -188,7 +187,7 @@ size_t decode_workspace(const Geometry& g, int H_q, int plan_len) {
 
 int32_t launch_decode(const Geometry& g, const CachePtrs& c, const uint16_t* q, int H_q, const int32_t* seq_len,
                       int plan_len, float scale, void* out, int out_mode, void* workspace, size_t ws_bytes,
-                      void* stream) {
+                      void* stream, float* const* push, int n_push) {
     using namespace dec;
     const int gq = H_q / g.H;
     const int GM = gq <= 4 ? 4 : 8;
@@ -202,6 +201,8 @@ int32_t launch_decode(const Geometry& g, const CachePtrs& c, const uint16_t* q, 
     a.scale_log2 = scale * 1.4426950408889634f;
     a.out = out;
     a.final_mode = out_mode;
+    a.push.n = n_push;
+    for (int i = 0; i < kMaxPush; ++i) a.push.p[i] = i < n_push ? push[i] : nullptr;
     if (kind >= 2) {
         // tensor-core kernel: stream-K over all (b, kv head) units, fused merge of units cut across CTAs
         const int n = plan_ctas(g, plan_len, in.occ, sms);
@@ -240,7 +241,8 @@ int32_t launch_decode(const Geometry& g, const CachePtrs& c, const uint16_t* q, 
     if (e != cudaSuccess) return fail(KVT_ERR_CUDA, "decode launch: %s", cudaGetErrorString(e));
     if (ns > 1) {
         int rows = g.B * H_q;
-        combine_kernel<<<(rows + 3) / 4, 128, 0, (cudaStream_t)stream>>>((const float*)workspace, ns, rows, out, out_mode);
+        combine_kernel<<<(rows + 3) / 4, 128, 0, (cudaStream_t)stream>>>((const float*)workspace, ns, rows, out, out_mode,
+                                                                          a.push);
         e = cudaGetLastError();
         if (e != cudaSuccess) return fail(KVT_ERR_CUDA, "combine launch: %s", cudaGetErrorString(e));
     }
@@ -251,7 +253,7 @@ int32_t launch_combine(const float* parts, int n_parts, int B, int H_q, int d, v
     using namespace dec;
     (void)d;
     int rows = B * H_q;
-    combine_kernel<<<(rows + 3) / 4, 128, 0, (cudaStream_t)stream>>>(parts, n_parts, rows, out, out_dtype);
+    combine_kernel<<<(rows + 3) / 4, 128, 0, (cudaStream_t)stream>>>(parts, n_parts, rows, out, out_dtype, PushList{});
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(KVT_ERR_CUDA, "combine launch: %s", cudaGetErrorString(e));
     return KVT_OK;

@@ -41,6 +41,24 @@ constexpr int kQStride = 36;       // padded floats per 32-channel block of q / 
 constexpr int kNG = 4;             // max channel groups per row (G = 32)
 constexpr unsigned kFull = 0xffffffffu;
 
+// Destinations of a pushed partial (a6 fused exchange, kvt_decode_attention_partial_push): each p[i] is a
+// [B][H_q][D + 2] fp32 block, typically this shard's slot of a peer GPU's gathered buffer (NVLink P2P).
+constexpr int kMaxPush = 8;
+struct PushList {
+    float* p[kMaxPush];
+    int n;
+};
+// (m, l, o) of one row element: c == 0 also stores m and l.  Writes to `out` (n == 0) or every push target.
+__device__ __forceinline__ void store_partial(const PushList& push, void* out, size_t row, int c, float M, float L,
+                                              float ov) {
+    const int n = push.n > 0 ? push.n : 1;
+    for (int i = 0; i < n; ++i) {
+        float* pr = (push.n > 0 ? push.p[i] : reinterpret_cast<float*>(out)) + row * (2 + D);
+        if (c == 0) { pr[0] = M; pr[1] = L; }
+        pr[2 + c] = ov;
+    }
+}
+
 struct DecodeArgs {
     Geometry g;
     CachePtrs c;
@@ -56,6 +74,7 @@ struct DecodeArgs {
     int final_mode;    // output mode of the fused combine (0, 1 or 2)
     unsigned long long* trace;   // KVT_TRACE builds only: per-CTA (SM, start, end); else null
     int n_cta;         // tensor-core kernel: stream-K CTAs (parts [n_cta][2][8][D + 2], counters [B][H_kv])
+    PushList push;     // out_mode 2 with push.n > 0: the partial rows go to every push.p[i] (a6 fused exchange)
 };
 
 // Stream-K cost of one (b, kv head) unit of the tensor-core kernel (kvt_decode_mma.cuh)
@@ -692,9 +711,7 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(DecodeArgs a) {
             if (c == 0) { pr[0] = M; pr[1] = L; }
             pr[2 + c] = L > 0.0f ? __fdiv_rn(O, L) : 0.0f;
         } else if (a.out_mode == 2) {
-            float* pr = reinterpret_cast<float*>(a.out) + row * (2 + D);
-            if (c == 0) { pr[0] = M; pr[1] = L; }
-            pr[2 + c] = L > 0.0f ? __fdiv_rn(O, L) : 0.0f;
+            store_partial(a.push, a.out, row, c, M, L, L > 0.0f ? __fdiv_rn(O, L) : 0.0f);
         } else {
             float o = L > 0.0f ? __fdiv_rn(O, L) : 0.0f;
             if (a.out_mode == 1) reinterpret_cast<float*>(a.out)[row * D + c] = o;

@@ -210,12 +210,11 @@ __device__ __forceinline__ void v_frag(const VRaw<VB>& r, int g4, uint32_t hA[4]
 }
 
 // Output row writer: mode 0 bf16, 1 fp32 (o = O / L), 2 partial (m, l, o).
-__device__ __forceinline__ void write_row(void* out, int mode, size_t row, int c, float M, float L, float O) {
+__device__ __forceinline__ void write_row(const DecodeArgs& a, void* out, int mode, size_t row, int c, float M, float L,
+                                          float O) {
     const float ov = L > 0.0f ? __fdiv_rn(O, L) : 0.0f;
     if (mode == 2) {
-        float* pr = reinterpret_cast<float*>(out) + row * (2 + D);
-        if (c == 0) { pr[0] = M; pr[1] = L; }
-        pr[2 + c] = ov;
+        dec::store_partial(a.push, out, row, c, M, L, ov);
     } else if (mode == 1) {
         reinterpret_cast<float*>(out)[row * D + c] = ov;
     } else {
@@ -966,7 +965,7 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
         }
         const size_t row = (size_t)b * a.H_q + (size_t)hk * gq + h;
         if (count == 1) {
-            write_row(a.out, a.out_mode, row, c, M, L, O);
+            write_row(a, a.out, a.out_mode, row, c, M, L, O);
         } else {
             float* pr = a.parts + ((size_t)(cta * 2 + slot) * 8 + h) * (2 + D);
             if (c == 0) { pr[0] = M; pr[1] = L; }
@@ -1001,7 +1000,7 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
                         O += wgt * __ldcg(pr + 2 + c);
                     }
                 }
-                write_row(a.out, a.out_mode, row, c, M, L, O);
+                write_row(a, a.out, a.out_mode, row, c, M, L, O);
             }
             if (tid == 0) a.counters[bh] = 0;
         }

@@ -74,6 +74,8 @@ def _load():
         "kvt_decode_attention": (i32, [ctypes.POINTER(_Cache), P, i32, P, P, ctypes.c_float, P, i32, P, u64, P]),
         "kvt_decode_attention_partial": (i32, [ctypes.POINTER(_Cache), P, i32, P, P, ctypes.c_float, P, P, u64,
                                                P]),
+        "kvt_decode_attention_partial_push": (i32, [ctypes.POINTER(_Cache), P, i32, P, P, ctypes.c_float,
+                                                    ctypes.POINTER(P), i32, P, u64, P]),
         "kvt_combine_partials": (i32, [P, i32, i32, i32, i32, P, i32, P]),
         "kvt_sensitivity_workspace_bytes": (i32, [i32, i32, i32, i32, i32, i32, ctypes.POINTER(u64)]),
         "kvt_layer_sensitivity": (i32, [i32, i32, i32, P, i32, i32, i32, P, P, i32, i32, i32, ctypes.c_float,
@@ -99,7 +101,8 @@ EXPORTED = ("kvt_abi_version", "kvt_status_string", "kvt_last_error", "kvt_confi
             "kvt_config_free", "kvt_validate_spec", "kvt_cache_buffer_sizes", "kvt_quantize_append",
             "kvt_decode_workspace_bytes", "kvt_decode_attention", "kvt_decode_attention_partial",
             "kvt_combine_partials", "kvt_sensitivity_workspace_bytes", "kvt_layer_sensitivity",
-            "kvt_pareto_prune", "kvt_dbscan", "kvt_prune_and_cluster", "kvt_search_space_log10", "kvt_page_bytes")
+            "kvt_pareto_prune", "kvt_dbscan", "kvt_prune_and_cluster", "kvt_search_space_log10", "kvt_page_bytes",
+            "kvt_decode_attention_partial_push")
 
 
 def lib():
@@ -324,6 +327,34 @@ def decode_attention_partial(cache: LayerCache, q: torch.Tensor, seq_len: torch.
                                              _ptr(seq_len), float(scale), _ptr(partial), _ptr(workspace),
                                              workspace.numel(), ctypes.c_void_p(_stream(stream))))
     return partial
+
+
+def decode_attention_partial_push(cache: LayerCache, q: torch.Tensor, seq_len: torch.Tensor, dsts,
+                                  seq_len_host=None, scale: Optional[float] = None,
+                                  workspace: Optional[torch.Tensor] = None, stream=None):
+    """a6 with the exchange fused into the kernel: the partial (m, l, o) rows [B][H_q][d + 2] are stored into
+    every destination of `dsts` (1..8 fp32 tensors, or raw device addresses, e.g. this shard's slot of each
+    peer's symmetric-memory gathered buffer)."""
+    _dev(q, "q", torch.bfloat16)
+    q = q.contiguous()
+    B, H_q, d = q.shape
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)
+    ptrs = []
+    for t in dsts:
+        if isinstance(t, torch.Tensor):
+            if t.dtype != torch.float32 or not t.is_cuda or not t.is_contiguous() or t.numel() < B * H_q * (d + 2):
+                raise ValueError("push destinations must be contiguous fp32 CUDA tensors of [B][H_q][d + 2]")
+            ptrs.append(t.data_ptr())
+        else:
+            ptrs.append(int(t))
+    arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
+    if workspace is None:
+        nb = decode_workspace_bytes(cache, H_q, seq_len_host)
+        workspace = torch.zeros(max(nb, 16), dtype=torch.uint8, device=q.device)
+    _check(_lib.kvt_decode_attention_partial_push(ctypes.byref(cache._c), _ptr(q), H_q, _host_i32(seq_len_host),
+                                                  _ptr(seq_len), float(scale), arr, len(ptrs), _ptr(workspace),
+                                                  workspace.numel(), ctypes.c_void_p(_stream(stream))))
 
 
 def combine_partials(gathered: torch.Tensor, out: Optional[torch.Tensor] = None, out_dtype=torch.float32,

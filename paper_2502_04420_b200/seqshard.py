@@ -11,6 +11,13 @@ there); the other ranks' specs use residual 0, i.e. every token they hold is qua
 
 The exchange is the only collective of the whole path; it moves B·H_q·(d + 2)·4 bytes per rank per
 layer (16.6 KB per sequence at Llama shape), so it is latency-bound.
+
+`SymmExchange` fuses the exchange into the attention kernel instead: the gathered
+buffer lives in symmetric memory, every rank's kernel stores its (m, l, o) rows straight into its slot of
+every peer's buffer over NVLink (kvt_decode_attention_partial_push), one device-side barrier orders the
+stores, and each rank combines its own buffer.  Two buffers alternate between layers, so one barrier per
+layer suffices (a rank can only overwrite a peer's buffer k again after that peer passed the next barrier,
+i.e. after its combine of buffer k).
 """
 from __future__ import annotations
 
@@ -63,3 +70,32 @@ def sharded_decode(cache, q: torch.Tensor, seq_len: torch.Tensor, seq_len_host=N
 
         return kvt.combine_partials(gathered, out_dtype=out_dtype)
     return combine_fn(gathered)
+
+
+class SymmExchange:
+    """Sequence-shard exchange over peer memory (no NCCL collective on the data path)."""
+
+    def __init__(self, shape, device, group=None):
+        import torch.distributed._symmetric_memory as symm_mem
+
+        self.group = group if group is not None else dist.group.WORLD
+        self.world = dist.get_world_size(self.group)
+        self.rank = dist.get_rank(self.group)
+        full = (2, self.world) + tuple(shape)                  # [buffer][shard][B][H_q][d + 2]
+        self.buf = symm_mem.empty(full, dtype=torch.float32, device=device)
+        self.handle = symm_mem.rendezvous(self.buf, self.group)
+        peers = [self.handle.get_buffer(p, full, torch.float32) for p in range(self.world)]
+        # slots[k][p] = this rank's slot of peer p's buffer k (a peer address mapped into this GPU)
+        self.slots = [[peers[p][k, self.rank] for p in range(self.world)] for k in range(2)]
+        self.k = 0
+
+    def decode(self, cache, q, seq_len, seq_len_host=None, scale=None, out=None, out_dtype=torch.bfloat16,
+               workspace=None, stream=None):
+        from . import kvt
+
+        k = self.k
+        kvt.decode_attention_partial_push(cache, q, seq_len, self.slots[k], seq_len_host=seq_len_host, scale=scale,
+                                          workspace=workspace, stream=stream)
+        self.handle.barrier(channel=0)
+        self.k ^= 1
+        return kvt.combine_partials(self.buf[k], out=out, out_dtype=out_dtype, stream=stream)
