@@ -75,3 +75,33 @@ def bf16_bits(t: torch.Tensor):
 
     assert t.dtype == torch.bfloat16
     return t.detach().contiguous().cpu().view(torch.int16).numpy().view(np.uint16)
+
+
+# ---- toy LLM (calibration with error accumulation): random weights and prompts only ----
+TOY_ARCH = {"L": 4, "d_model": 256, "H_q": 4, "H_kv": 2, "D": 128, "vocab": 256, "d_ff": 512}
+ATTN_GAIN = 4.0          # attention output gain: the residual stream is attention-dominated (tokens depend on the KV)
+
+
+def toy_weights(seed: int, arch=None):
+    """fp32 CPU weights of the toy decoder (N(0, 1/fan_in)); the key projection's output channels
+    c = 0 (mod 8) of every head are scaled x11, the key-outlier recipe above."""
+    a = dict(TOY_ARCH if arch is None else arch)
+    g = generator(seed, "cpu")
+    dm, D = a["d_model"], a["D"]
+
+    def w(n_in, n_out):
+        return torch.randn(n_in, n_out, generator=g) / n_in ** 0.5
+
+    out = {"emb": torch.randn(a["vocab"], dm, generator=g), "layers": []}
+    for _ in range(a["L"]):
+        wk = w(dm, a["H_kv"] * D)
+        wk.view(dm, a["H_kv"], D)[..., ::OUTLIER_PERIOD] *= OUTLIER_SCALE
+        out["layers"].append({"wq": w(dm, a["H_q"] * D), "wk": wk, "wv": w(dm, a["H_kv"] * D),
+                              "wo": ATTN_GAIN * w(a["H_q"] * D, dm), "w1": w(dm, a["d_ff"]), "w2": w(a["d_ff"], dm)})
+    out["unemb"] = w(dm, a["vocab"])
+    return out
+
+
+def toy_prompts(seed: int, batch: int, length: int, vocab: int = TOY_ARCH["vocab"]) -> torch.Tensor:
+    """int64 [batch][length] token ids."""
+    return torch.randint(0, vocab, (batch, length), generator=generator(seed, "cpu"))
