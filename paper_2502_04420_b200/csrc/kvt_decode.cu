@@ -220,7 +220,21 @@ int32_t launch_decode(const Geometry& g, const CachePtrs& c, const uint16_t* q, 
         cudaMemsetAsync(g_trace, 0, sizeof(unsigned long long) * 11 * 4096, (cudaStream_t)stream);
         a.trace = g_trace;
 #endif
-        in.fn<<<n, kThreads, in.smem, (cudaStream_t)stream>>>(a);
+        // programmatic dependent launch: the kernel's prologue (length scan, q setup) may overlap the tail of
+        // the preceding kernel in the stream (the append of the same layer, which triggers its dependents at
+        // entry); the kernel waits (griddepcontrol.wait) before its first read of the cache
+        static const bool pdl = [] { const char* e = getenv("KVT_PDL"); return !e || atoi(e) != 0; }();
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(n);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = in.smem;
+        cfg.stream = (cudaStream_t)stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = pdl ? 1 : 0;
+        cudaLaunchKernelEx(&cfg, in.fn, a);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return fail(KVT_ERR_CUDA, "decode launch: %s", cudaGetErrorString(e));
         return KVT_OK;

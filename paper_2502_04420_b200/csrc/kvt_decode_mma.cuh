@@ -325,49 +325,6 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
     const int n_my = tile_hi - tile_lo - warp > 0 ? (tile_hi - tile_lo - warp + kWarps - 1) / kWarps : 0;
     // ---- stage the tail rows [n_main, S) into shared memory with bulk copies (one round trip instead of a
     // dependent global load per token group); `tl` then addresses them with the cache's own indexing ----
-    Slice tl = sl;
-    if (a.c.bt) {
-        tl.bt = a.c.bt + (size_t)b * a.c.max_pages;
-        tl.pstride = (size_t)g.H * g.rec;
-    }
-    uint64_t* tbar = reinterpret_cast<uint64_t*>(smem + Gm::Q_BYTES + Gm::TAIL_PART);
-    bool staged = false;
-    if (KVT_EXP != 5 && do_tail && n_main < S) {
-        const int kq = nqK < S ? nqK : S, vq = nqV < S ? nqV : S;
-        const int q_hi = kq > vq ? kq : vq;                               // quantised tail tokens end here
-        const int r0 = n_main / kTile, r1 = (q_hi + kTile - 1) / kTile;  // their tile records
-        const uint32_t b_rec = q_hi > n_main ? (uint32_t)(r1 - r0) * Gm::STAGE : 0u;
-        // K residual: KIVI linear slots [0, S - nqK); per-token keys: the whole ring (slot t mod R)
-        const uint32_t b_kr = KPT ? (kq < S ? (uint32_t)g.R * D * 2 : 0u) : (uint32_t)(S - kq) * D * 2;
-        const uint32_t b_vr = (vq < S && sl.vr) ? (uint32_t)g.R * D * 2 : 0u;
-        const uint32_t total = b_rec + b_kr + b_vr;                       // all multiples of 16
-        if (Gm::SCRATCH_BYTES + total <= (uint32_t)Gm::BODY) {
-            staged = true;
-            uint8_t* p_rec = body + Gm::SCRATCH_BYTES;
-            uint8_t* p_kr = p_rec + b_rec;
-            uint8_t* p_vr = p_kr + b_kr;
-            if (tid == 0) {
-                mbar_init(tbar);
-                asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-                fence_proxy_async();
-                mbar_expect_tx(tbar, total);
-                if (b_rec) {
-                    if (tl.bt) {
-                        for (int r = r0; r < r1; ++r) bulk_g2s(p_rec + (size_t)(r - r0) * Gm::STAGE, tl.recp(r, g), Gm::STAGE, tbar);
-                    } else {
-                        bulk_g2s(p_rec, sl.kc + (size_t)r0 * Gm::STAGE, b_rec, tbar);
-                    }
-                }
-                if (b_kr) bulk_g2s(p_kr, sl.kr, b_kr, tbar);
-                if (b_vr) bulk_g2s(p_vr, sl.vr, b_vr, tbar);
-            }
-            // virtual bases: record r of the cache lands at its staged copy under the cache's own indexing
-            tl.kc = p_rec - (size_t)r0 * Gm::STAGE;
-            tl.bt = nullptr;
-            tl.kr = reinterpret_cast<const uint16_t*>(p_kr);
-            tl.vr = reinterpret_cast<const uint16_t*>(p_vr);
-        }
-    }
     // softmax heads of this thread (the QK D columns it holds after the hi/lo fold)
     const int hA = (GM == 8) ? 2 * tig : 2 * (tig & 1);
     // ---- per-head power-of-two scale of q (max |q 2^qa| in [64, 128)), computed once per CTA ----
@@ -416,6 +373,53 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
                 }
                 qg[gg][j] = acc;
             }
+    }
+    // Everything above reads only q and the lengths, which the producer of q wrote before the append kernel
+    // that precedes this launch started; the launch is a programmatic dependent of that append (PDL), so
+    // the prologue above overlaps it.  The cache (records, residuals) is read only after the wait.
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    Slice tl = sl;
+    if (a.c.bt) {
+        tl.bt = a.c.bt + (size_t)b * a.c.max_pages;
+        tl.pstride = (size_t)g.H * g.rec;
+    }
+    uint64_t* tbar = reinterpret_cast<uint64_t*>(smem + Gm::Q_BYTES + Gm::TAIL_PART);
+    bool staged = false;
+    if (KVT_EXP != 5 && do_tail && n_main < S) {
+        const int kq = nqK < S ? nqK : S, vq = nqV < S ? nqV : S;
+        const int q_hi = kq > vq ? kq : vq;                               // quantised tail tokens end here
+        const int r0 = n_main / kTile, r1 = (q_hi + kTile - 1) / kTile;  // their tile records
+        const uint32_t b_rec = q_hi > n_main ? (uint32_t)(r1 - r0) * Gm::STAGE : 0u;
+        // K residual: KIVI linear slots [0, S - nqK); per-token keys: the whole ring (slot t mod R)
+        const uint32_t b_kr = KPT ? (kq < S ? (uint32_t)g.R * D * 2 : 0u) : (uint32_t)(S - kq) * D * 2;
+        const uint32_t b_vr = (vq < S && sl.vr) ? (uint32_t)g.R * D * 2 : 0u;
+        const uint32_t total = b_rec + b_kr + b_vr;                       // all multiples of 16
+        if (Gm::SCRATCH_BYTES + total <= (uint32_t)Gm::BODY) {
+            staged = true;
+            uint8_t* p_rec = body + Gm::SCRATCH_BYTES;
+            uint8_t* p_kr = p_rec + b_rec;
+            uint8_t* p_vr = p_kr + b_kr;
+            if (tid == 0) {
+                mbar_init(tbar);
+                asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+                fence_proxy_async();
+                mbar_expect_tx(tbar, total);
+                if (b_rec) {
+                    if (tl.bt) {
+                        for (int r = r0; r < r1; ++r) bulk_g2s(p_rec + (size_t)(r - r0) * Gm::STAGE, tl.recp(r, g), Gm::STAGE, tbar);
+                    } else {
+                        bulk_g2s(p_rec, sl.kc + (size_t)r0 * Gm::STAGE, b_rec, tbar);
+                    }
+                }
+                if (b_kr) bulk_g2s(p_kr, sl.kr, b_kr, tbar);
+                if (b_vr) bulk_g2s(p_vr, sl.vr, b_vr, tbar);
+            }
+            // virtual bases: record r of the cache lands at its staged copy under the cache's own indexing
+            tl.kc = p_rec - (size_t)r0 * Gm::STAGE;
+            tl.bt = nullptr;
+            tl.kr = reinterpret_cast<const uint16_t*>(p_kr);
+            tl.vr = reinterpret_cast<const uint16_t*>(p_vr);
+        }
     }
     __syncthreads();
     // GM == 4: lanes tig and tig^2 hold the same probabilities, so they prepare different value groups:

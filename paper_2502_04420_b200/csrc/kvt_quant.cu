@@ -201,6 +201,9 @@ __device__ void per_channel_key(int phase, int bits, int G, int F, int L0, int S
 }
 
 __global__ void __launch_bounds__(kWarps * 32) append_kernel(AppendArgs a) {
+    // the decode attention launched next may start its q/length prologue now (it waits for this grid's
+    // completion before reading the cache: griddepcontrol.wait in decode_mma_kernel)
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     const int b = blockIdx.z, h = blockIdx.y, chunk = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int n = a.n_new[b];
