@@ -163,9 +163,13 @@ static int plan_ctas(const Geometry& g, int plan_len, int occ, int sms) {
     const long long units = (long long)g.B * g.H;
     const long long C = units * dec::unit_cost(g, plan_len).cost;
     const long long slots = (long long)occ * sms;
-    // whole units when they (nearly) fill the wave: no unit is cut, no merge (measured: 512 units of 255
-    // tiles on 592 slots run 2.5% faster uncut than cut into 592 equal shares)
-    if (units <= slots && 4 * units >= 3 * slots) return (int)units;
+    // Whole units (no cut, no merge) when they fit one wave, give most SMs at least two CTAs, and the
+    // busiest SM holds at most 1.2x the average: cutting a unit costs more than that imbalance
+    // (measured, one layer at 8k: Qwen 256 units on 444 slots 108.5 us uncut vs 117.8 us stream-K, per-token
+    // K8V2 99 vs 118 us; Llama 512 units on 592 slots 2.5% faster uncut; but 160 units: stream-K 22% faster,
+    // 128 units: 12% faster — a single 4-warp CTA cannot keep an SM busy).
+    const long long per_sm = (units + sms - 1) / sms;
+    if (units <= slots && 2 * units >= 3LL * sms && 5 * per_sm * sms <= 6 * units) return (int)units;
     long long n = (C + 15) / 16;                        // cut units only into pieces of >= ~16 work units
     if (n < units) n = units;                           // ... but never leave whole units waiting in line
     if (n > slots) n = slots;
@@ -223,7 +227,11 @@ int32_t launch_decode(const Geometry& g, const CachePtrs& c, const uint16_t* q, 
         // programmatic dependent launch: the kernel's prologue (length scan, q setup) may overlap the tail of
         // the preceding kernel in the stream (the append of the same layer, which triggers its dependents at
         // entry); the kernel waits (griddepcontrol.wait) before its first read of the cache
-        static const bool pdl = [] { const char* e = getenv("KVT_PDL"); return !e || atoi(e) != 0; }();
+        // Only when the grid (nearly) fills the wave: CTAs dispatched while the append still occupies SMs are
+        // placed unevenly, which a partial wave cannot absorb (Qwen, 256 whole units on 444 slots: 15 449
+        // tokens/s with PDL vs 19 583 without; Llama, 512 on 592: +2% with PDL).
+        static const bool pdl_env = [] { const char* e = getenv("KVT_PDL"); return !e || atoi(e) != 0; }();
+        const bool pdl = pdl_env && 4LL * n >= 3LL * in.occ * sms;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(n);
         cfg.blockDim = dim3(kThreads);
