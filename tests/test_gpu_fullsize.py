@@ -59,3 +59,31 @@ def test_fullsize_sampled(kvt, oracle, kb, vb, H, g, B):
                                       kvt_synth.bf16_bits(q[b, h * g:(h + 1) * g]), 1 / math.sqrt(D))
         err = rel_row_err(out[b, h * g:(h + 1) * g].cpu().numpy(), ref)
         assert err.max() <= TOL, f"(b={b}, h={h}): normalised error {err.max():.2e}"
+
+
+@pytest.mark.parametrize("H,g", [(4, 7), (8, 4)])
+def test_whole_unit_plan_ragged(kvt, oracle, H, g):
+    """The whole-unit work plan (B = 64: 256 or 512 units fill most SMs twice or more) with ragged lengths:
+    unit costs differ, so the equal-cost ranges cut units and the last CTA of each merges them."""
+    B = 64
+    lens = kvt_synth.ragged_lengths(B, 1, 1500, seed=77).tolist()
+    spec = kvt.LayerSpec.kivi(4, 4)
+    cap = 1536
+    dev = torch.device("cuda")
+    K = kvt_synth.keys((B, H, cap, D), seed=78).to(dev)
+    V = kvt_synth.values((B, H, cap, D), seed=79).to(dev)
+    q = kvt_synth.queries((B, H * g, D), seed=80).to(dev)
+    cache = kvt.LayerCache(spec, B, H, D, cap)
+    kvt.quantize_append(cache, K, V, torch.zeros(B, dtype=torch.int32, device=dev),
+                        torch.tensor(lens, dtype=torch.int32, device=dev), len_before_host=[0] * B, n_new_host=lens)
+    sl = torch.tensor(lens, dtype=torch.int32, device=dev)
+    out = kvt.decode_attention(cache, q, sl, seq_len_host=lens, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(H)
+    for b in rng.choice(B, 24, replace=False):
+        h = int(rng.integers(H))
+        S = lens[b]
+        ref = oracle.decode_reference(spec.mode, 4, 4, 32, 32, D, kvt_synth.bf16_bits(K[b, h, :S]),
+                                      kvt_synth.bf16_bits(V[b, h, :S]), kvt_synth.bf16_bits(q[b, h * g:(h + 1) * g]),
+                                      1 / math.sqrt(D))
+        assert rel_row_err(out[b, h * g:(h + 1) * g].cpu().numpy(), ref).max() <= TOL, (b, h, S)
