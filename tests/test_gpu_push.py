@@ -4,8 +4,6 @@ peer's symmetric-memory buffer over NVLink).  On one GPU: the pushed rows equal 
 bit in every destination, for the tensor-core kernel (fused in-kernel merge) and the generic kernel
 (separate combine launch); and the symmetric-memory exchange on a one-rank NCCL group reproduces the
 unsharded decode."""
-import math
-import os
 import socket
 
 import pytest
