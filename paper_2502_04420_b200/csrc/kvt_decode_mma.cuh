@@ -243,7 +243,7 @@ struct Geo {
     static constexpr int SH_OFF = W_OFF + W_BYTES;
     static constexpr int SH_STRIDE = 20;                          // words per tig row (16 used; padding: no bank conflicts)
     static constexpr int BAR_OFF = SH_OFF + 4 * SH_STRIDE * 4;    // one mbarrier per stage
-    static constexpr int WARP_BYTES = BAR_OFF + 8 * NS;
+    static constexpr int WARP_BYTES = (BAR_OFF + 8 * NS + 15) / 16 * 16;
     static constexpr int Q_BYTES = GM * D * 4;           // q fp32 [GM][128]
     static constexpr int TAIL_PART = ((GM * (2 + D) * 4) + 15) / 16 * 16;    // tail partial (m, l, o) [GM]
     static constexpr int TAIL_BYTES = TAIL_PART + 16;                          // + the tail-staging mbarrier
