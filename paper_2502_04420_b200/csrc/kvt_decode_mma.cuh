@@ -986,7 +986,46 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
             is_last = (old == count - 1);
         }
         __syncthreads();
-        if (is_last) {
+        if (is_last && count * 8 * 2 * (int)sizeof(float) <= Gm::BODY) {
+            // (m, l) of every (partial, head) staged in shared memory by all threads at once, then the o loads
+            // of all heads of a partial issued together: no chain of dependent L2 round trips per head
+            __threadfence();
+            float* ml = reinterpret_cast<float*>(body);        // [count][8 heads][m, l]; body is free here
+            for (int i = tid; i < count * 8; i += kThreads) {
+                const int k = i >> 3, h = i & 7;
+                if (h < gq) {
+                    const float* pr = a.parts + ((size_t)((c_first + k) * 2 + (k == 0)) * 8 + h) * (2 + D);
+                    ml[2 * i] = __ldcg(pr);
+                    ml[2 * i + 1] = __ldcg(pr + 1);
+                }
+            }
+            __syncthreads();
+            float Mh[8], Lh[8], Oh[8];
+#pragma unroll
+            for (int h = 0; h < 8; ++h) {
+                Mh[h] = -INFINITY; Lh[h] = 0.0f; Oh[h] = 0.0f;
+                if (h < gq)
+                    for (int k = 0; k < count; ++k) Mh[h] = fmaxf(Mh[h], ml[2 * (k * 8 + h)]);
+            }
+            for (int k = 0; k < count; ++k) {
+                const float* pk = a.parts + ((size_t)((c_first + k) * 2 + (k == 0)) * 8) * (2 + D) + 2 + c;
+#pragma unroll
+                for (int h = 0; h < 8; ++h) {
+                    if (h < gq && Mh[h] != -INFINITY) {
+                        const float l = ml[2 * (k * 8 + h) + 1];
+                        if (l != 0.0f) {
+                            const float wgt = l * fexp2(ml[2 * (k * 8 + h)] - Mh[h]);
+                            Lh[h] += wgt;
+                            Oh[h] += wgt * __ldcg(pk + (size_t)h * (2 + D));
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int h = 0; h < 8; ++h)
+                if (h < gq) write_row(a, a.out, a.out_mode, (size_t)b * a.H_q + (size_t)hk * gq + h, c, Mh[h], Lh[h], Oh[h]);
+            if (tid == 0) a.counters[bh] = 0;
+        } else if (is_last) {
             __threadfence();
             for (int h = 0; h < gq; ++h) {
                 const size_t row = (size_t)b * a.H_q + (size_t)hk * gq + h;
