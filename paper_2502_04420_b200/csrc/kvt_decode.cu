@@ -17,9 +17,9 @@ KFn get_decode_k2(int VB, bool KPC, int GM);
 KFn get_decode_k4(int VB, bool KPC, int GM);
 KFn get_decode_k8(int VB, bool KPC, int GM);
 KFn get_decode_k16(int VB, bool KPC, int GM);
-KFn get_decode_mma_k2(int VB, int GM, bool kpt, size_t* smem);
-KFn get_decode_mma_k4(int VB, int GM, bool kpt, size_t* smem);
-KFn get_decode_mma_k8(int VB, int GM, bool kpt, size_t* smem);
+KFn get_decode_mma_k2(int VB, int GM, bool kpt, bool paged, size_t* smem);
+KFn get_decode_mma_k4(int VB, int GM, bool kpt, bool paged, size_t* smem);
+KFn get_decode_mma_k8(int VB, int GM, bool kpt, bool paged, size_t* smem);
 
 // K3: merge n_parts partial rows [n_parts][rows][2 + D] -> out (bf16 / fp32 / partial).  One warp
 // per row; lane owns 4 channels.
@@ -80,24 +80,25 @@ static int bits_index(int b) { return b == 2 ? 0 : b == 4 ? 1 : b == 8 ? 2 : 3; 
 
 // Per-device cache of (function, smem, occupancy) for each instance; configured once.
 static std::mutex g_mu;
-static Instance g_inst[8][4][4][4][2];   // [device][kb][vb][kind: 0/1 generic per-token/per-channel, 2/3 mma KIVI/per-token][gm]
-static bool g_ready[8][4][4][4][2];
+static Instance g_inst[8][4][4][4][2][2];   // [device][kb][vb][kind: 0/1 generic per-token/per-channel, 2/3 mma KIVI/per-token][gm][paged]
+static bool g_ready[8][4][4][4][2][2];
 static int g_sms[8];
 
 // kind: 0 = generic CUDA-core kernel (per-token key), 1 = generic (per-channel key), 2 = tensor-core KIVI
-static int32_t get_instance(int kb, int vb, int kind, int GM, Instance* out, int* sms) {
+static int32_t get_instance(int kb, int vb, int kind, int GM, Instance* out, int* sms, bool paged = false) {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 8) return fail(KVT_ERR_CUDA, "cudaGetDevice failed");
     int ki = bits_index(kb), vi = bits_index(vb), gi = GM == 4 ? 0 : 1;
     std::lock_guard<std::mutex> lk(g_mu);
-    if (!g_ready[dev][ki][vi][kind][gi]) {
+    const int pi = paged && kind >= 2 ? 1 : 0;
+    if (!g_ready[dev][ki][vi][kind][gi][pi]) {
         Instance in;
         if (kind >= 2) {
             const bool kpt = kind == 3;
             switch (kb) {
-                case 2: in.fn = get_decode_mma_k2(vb, GM, kpt, &in.smem); break;
-                case 4: in.fn = get_decode_mma_k4(vb, GM, kpt, &in.smem); break;
-                default: in.fn = get_decode_mma_k8(vb, GM, kpt, &in.smem); break;
+                case 2: in.fn = get_decode_mma_k2(vb, GM, kpt, paged, &in.smem); break;
+                case 4: in.fn = get_decode_mma_k4(vb, GM, kpt, paged, &in.smem); break;
+                default: in.fn = get_decode_mma_k8(vb, GM, kpt, paged, &in.smem); break;
             }
         } else {
             const bool kpc = kind == 1;
@@ -118,10 +119,10 @@ static int32_t get_instance(int kb, int vb, int kind, int GM, Instance* out, int
             cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
             g_sms[dev] = n > 0 ? n : 148;
         }
-        g_inst[dev][ki][vi][kind][gi] = in;
-        g_ready[dev][ki][vi][kind][gi] = true;
+        g_inst[dev][ki][vi][kind][gi][pi] = in;
+        g_ready[dev][ki][vi][kind][gi][pi] = true;
     }
-    *out = g_inst[dev][ki][vi][kind][gi];
+    *out = g_inst[dev][ki][vi][kind][gi][pi];
     *sms = g_sms[dev];
     return KVT_OK;
 }
@@ -196,7 +197,7 @@ int32_t launch_decode(const Geometry& g, const CachePtrs& c, const uint16_t* q, 
     const int gq = H_q / g.H;
     const int GM = gq <= 4 ? 4 : 8;
     Instance in; int sms = 148;
-    int32_t st = get_instance(g.kb, g.vb, kernel_kind(g), GM, &in, &sms);
+    int32_t st = get_instance(g.kb, g.vb, kernel_kind(g), GM, &in, &sms, c.bt != nullptr);
     if (st) return st;
     const int kind = kernel_kind(g);
     if (g.B > 65535 || g.H > 65535) return fail(KVT_ERR_UNSUPPORTED, "decode: batch/heads exceed grid limits");

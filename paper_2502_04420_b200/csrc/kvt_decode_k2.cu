@@ -29,21 +29,26 @@ KFn get_decode_k2(int VB, bool KPC, int GM) {
 // tensor-core instances (G = 32 tile records): returns the kernel and its dynamic shared memory.
 // KPT (per-token keys): q needs no hi/lo split, so with g <= 4 the 8 columns hold the 4 heads twice (the
 // lanes tig and tig ^ 2 then see the same heads, as after the KIVI hi/lo fold).
-template <int VB>
+template <int VB, bool P>
 static KFn mma_pick(int GM, bool kpt, size_t* smem) {
-    if (kpt && GM == 4) { *smem = mma::Geo<2, VB, 4>::SMEM; return mma::decode_mma_kernel<2, VB, 4, true>; }
-    if (kpt) { *smem = mma::Geo<2, VB, 8>::SMEM; return mma::decode_mma_kernel<2, VB, 8, true>; }
-    if (GM == 4) { *smem = mma::Geo<2, VB, 4>::SMEM; return mma::decode_mma_kernel<2, VB, 4, false>; }
+    if (kpt && GM == 4) { *smem = mma::Geo<2, VB, 4>::SMEM; return mma::decode_mma_kernel<2, VB, 4, true, P>; }
+    if (kpt) { *smem = mma::Geo<2, VB, 8>::SMEM; return mma::decode_mma_kernel<2, VB, 8, true, P>; }
+    if (GM == 4) { *smem = mma::Geo<2, VB, 4>::SMEM; return mma::decode_mma_kernel<2, VB, 4, false, P>; }
     *smem = mma::Geo<2, VB, 8>::SMEM;
-    return mma::decode_mma_kernel<2, VB, 8, false>;
+    return mma::decode_mma_kernel<2, VB, 8, false, P>;
 }
 
-KFn get_decode_mma_k2(int VB, int GM, bool kpt, size_t* smem) {
+template <bool P>
+static KFn mma_pick_vb(int VB, int GM, bool kpt, size_t* smem) {
     switch (VB) {
-        case 2: return mma_pick<2>(GM, kpt, smem);
-        case 4: return mma_pick<4>(GM, kpt, smem);
-        default: return mma_pick<8>(GM, kpt, smem);
+        case 2: return mma_pick<2, P>(GM, kpt, smem);
+        case 4: return mma_pick<4, P>(GM, kpt, smem);
+        default: return mma_pick<8, P>(GM, kpt, smem);
     }
+}
+
+KFn get_decode_mma_k2(int VB, int GM, bool kpt, bool paged, size_t* smem) {
+    return paged ? mma_pick_vb<true>(VB, GM, kpt, smem) : mma_pick_vb<false>(VB, GM, kpt, smem);
 }
 
 }  // namespace dec

@@ -280,7 +280,7 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 // do_tail).  count == 1: the segment is the whole unit and writes the output row; otherwise it leaves a
 // partial in parts slot (cta, slot) and the last of the unit's `count` CTAs (c_first ...) merges them.
 // GM: 4 (g <= 4: n = 4 heads x {hi, lo}) or 8 (g <= 8: separate hi and lo MMAs).
-template <int KB, int VB, int GM, bool KPT>
+template <int KB, int VB, int GM, bool KPT, bool PAGED>
 __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, const int b, const int hk,
                                         const int tile_lo, const int tile_hi, const bool do_tail, const int cta,
                                         const int slot, const int c_first, const int count) {
@@ -312,7 +312,7 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
     Slice sl;
     // paged: kc = the pool base of head hk and record j is page bt[b][j] (read from the kernel parameters
     // where used, so the main loop keeps no extra registers)
-    sl.kc = a.c.bt ? a.c.k_codes + (size_t)hk * g.rec : a.c.k_codes + bh * g.kc;
+    sl.kc = PAGED ? a.c.k_codes + (size_t)hk * g.rec : a.c.k_codes + bh * g.kc;
     sl.km = nullptr;                                 // tile records: K meta, V codes and V meta live in kc
     sl.kr = a.c.k_resid + bh * (g.kr / 2);
     sl.vc = nullptr;
@@ -379,7 +379,7 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
     // the prologue above overlaps it.  The cache (records, residuals) is read only after the wait.
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     Slice tl = sl;
-    if (a.c.bt) {
+    if (PAGED) {
         tl.bt = a.c.bt + (size_t)b * a.c.max_pages;
         tl.pstride = (size_t)g.H * g.rec;
     }
@@ -576,8 +576,8 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
         const int t0 = (tile_lo + warp + it * kWarps) * kTile;
         uint8_t* sb = wbase + st * Gm::STAGE;
         mbar_expect_tx(bars + st, Gm::STAGE);
-        const uint8_t* src = a.c.bt ? a.c.k_codes + ((size_t)a.c.bt[(size_t)b * a.c.max_pages + t0 / kTile] * g.H + hk) * Gm::STAGE
-                                    : sl.kc + (size_t)(t0 / kTile) * Gm::STAGE;
+        const uint8_t* src = PAGED ? a.c.k_codes + ((size_t)a.c.bt[(size_t)b * a.c.max_pages + t0 / kTile] * g.H + hk) * Gm::STAGE
+                                   : sl.kc + (size_t)(t0 / kTile) * Gm::STAGE;
         bulk_g2s(sb, src, Gm::STAGE, bars + st);     // one tile record
     };
 
@@ -1061,7 +1061,8 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
 // the CTA whose range [c C / n, (c + 1) C / n) holds position x
 __device__ __forceinline__ int cta_of(long long x, long long C, int n) { return (int)(((x + 1) * n - 1) / C); }
 
-template <int KB, int VB, int GM, bool KPT>
+// PAGED: tile records addressed through the block table (compile-time, so the dense issue path stays short)
+template <int KB, int VB, int GM, bool KPT, bool PAGED>
 __global__ void __launch_bounds__(kThreads, GM == 4 ? 4 : 3) decode_mma_kernel(DecodeArgs a) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ long long s_wsum[kWarps];
@@ -1114,7 +1115,7 @@ __global__ void __launch_bounds__(kThreads, GM == 4 ? 4 : 3) decode_mma_kernel(D
         const int x0 = (int)(pos - Pu);
         const int x1 = (int)(hi - Pu < uc.cost ? hi - Pu : uc.cost);
         const int cf = cta_of(Pu, C, n), cl = cta_of(Pu + uc.cost - 1, C, n);
-        segment<KB, VB, GM, KPT>(a, smem, b, hk, min(x0, uc.tiles), min(x1, uc.tiles), x1 == uc.cost, cta,
+        segment<KB, VB, GM, KPT, PAGED>(a, smem, b, hk, min(x0, uc.tiles), min(x1, uc.tiles), x1 == uc.cost, cta,
                             cta == cf ? 1 : 0, cf, cl - cf + 1);
         pos = Pu + x1;
         __syncthreads();                                    // the next segment reuses shared memory
