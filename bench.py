@@ -378,6 +378,8 @@ def run_kvt(args):
         step()
     end.record(stream)
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     # roofline pass: the next K steps again, with CUDA events around every attention launch
     for i in range(args.steps):
         step(evs[i])
@@ -458,6 +460,8 @@ def run_kvt(args):
         e2e_run(args.steps)
         e2.record(stream)
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         ems = s2.elapsed_time(e2)
         if world > 1:
             t = torch.tensor([ems], device=dev, dtype=torch.float64)
