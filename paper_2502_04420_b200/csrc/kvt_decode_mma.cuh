@@ -622,13 +622,14 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
             const int sbx = 7 - frexp_e(bf2f(smb));
             const float ssc = pow2(sbx);
             ks_inv = pow2(-sbx);
-            __half* shh = reinterpret_cast<__half*>(sh_s);
+            // channel 4 lane + e sits at half index idx0 + 2e (K2, K4) or idx0 + e (K8) of the slot table (the
+            // KSlots order), so one base per lane and immediate offsets
+            const int code0 = k_slot_of<KB>((4 * lane) & 31);
+            __half* shh = reinterpret_cast<__half*>(sh_s) + ((lane >> 3) * Gm::SH_STRIDE + (code0 >> 1)) * 2 + (code0 & 1);
             float z[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                const int c = 4 * lane + e;
-                const int code = k_slot_of<KB>(c & 31);
-                shh[((c >> 5) * Gm::SH_STRIDE + (code >> 1)) * 2 + (code & 1)] = __float2half_rn(bf2f(mw[e] & 0xffffu) * ssc);
+                shh[KB == 8 ? e : 2 * e] = __float2half_rn(bf2f(mw[e] & 0xffffu) * ssc);
                 z[e] = bf2f(mw[e] >> 16);
             }
             // bias partials of the GM heads, reduce-scattered: lane l ends with head (l & 7)
