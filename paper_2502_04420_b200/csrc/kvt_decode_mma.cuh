@@ -643,11 +643,12 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
                     bz[h] = 0.0f;
                 }
             }
-            {
+            // GM == 8: scatter over lane bits 2, 1, 0 (lane l ends with head l & 7), then sum over bits 3, 4.
+            // GM == 4: scatter over bits 1, 0 only (lane l ends with head l & 3), then sum over bits 2, 3, 4.
+            if constexpr (GM == 8) {
                 const bool up = (lane >> 2) & 1;
 #pragma unroll
                 for (int h = 0; h < 4; ++h) {
-                    if (h + 4 >= GM && h >= GM) continue;
                     const float recv = __shfl_xor_sync(kFull, up ? bz[h] : bz[h + 4], 4);
                     bz[h] = (up ? bz[h + 4] : bz[h]) + recv;
                 }
@@ -665,6 +666,7 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
                 const float recv = __shfl_xor_sync(kFull, up ? bz[0] : bz[1], 1);
                 bz[0] = (up ? bz[1] : bz[0]) + recv;
             }
+            if constexpr (GM == 4) bz[0] += __shfl_xor_sync(kFull, bz[0], 4);
             bz[0] += __shfl_xor_sync(kFull, bz[0], 8);
             bz[0] += __shfl_xor_sync(kFull, bz[0], 16);
             bias[0] = __shfl_sync(kFull, bz[0], hA);
