@@ -431,9 +431,11 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
     // ---- running state ----
     float m_run[2] = {-INFINITY, -INFINITY};              // reference max (lazy: moves only by > 8)
     float l_part[2] = {0.0f, 0.0f};
-    float zacc[4][2];
+    // value zero-point sums per (group, head), kept as two partials (token rows r = 0, 1) so that the FFMA2
+    // operand pairs are the (p(T), p(T+8)) pairs the weights use as well: no register moves
+    float2 zacc2[4][2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) zacc[i][0] = zacc[i][1] = 0.0f;
+    for (int i = 0; i < 4; ++i) zacc2[i][0] = zacc2[i][1] = make_float2(0.0f, 0.0f);
     float o[8][4];                 // PV accumulators: m-tile (γ, μ) = 2γ + μ
 #pragma unroll
     for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.0f;
@@ -852,11 +854,16 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
 #pragma unroll
                 for (int j = 0; j < 2; ++j)
                     pk[mt][j] = dec::fmul2(make_float2(p[mt][0][j], p[mt][1][j]), make_float2(ksc, ksc));
+            // weight-tile word of (group gsh + gr, m-tile mt): one per-lane base plus a compile-time offset (gsh is
+            // even, so 4 ((gsh + gr) >> 1) = 4 (gsh >> 1) for GM == 4; gsh = 0 for GM == 8)
+            uint32_t* const wst = w_s + (gsh * 2 * 8 + gid) * 8 + 4 * (gsh >> 1) + hA;
 #pragma unroll
             for (int gr = 0; gr < NGL; ++gr) {
-                const int gam = gsh + gr;
-                float2 za = make_float2(zacc[gr][0], zacc[gr][1]);
-                if (resc) za = dec::fmul2(za, make_float2(alpha[0], alpha[1]));
+                float2 za0 = zacc2[gr][0], za1 = zacc2[gr][1];
+                if (resc) {
+                    za0 = dec::fmul2(za0, make_float2(alpha[0], alpha[0]));
+                    za1 = dec::fmul2(za1, make_float2(alpha[1], alpha[1]));
+                }
 #pragma unroll
                 for (int mt = 0; mt < 2; ++mt) {
                     const uint32_t w0 = mw[mt][0][gr], w1 = mw[mt][1][gr];
@@ -865,13 +872,13 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
                     const float2 wa = dec::fmul2(pk[mt][0], sv), wb = dec::fmul2(pk[mt][1], sv);
                     wv.x = h2u(__floats2half2_rn(wa.x, wa.y));
                     wv.y = h2u(__floats2half2_rn(wb.x, wb.y));
-                    *reinterpret_cast<uint2*>(w_s + ((gam * 2 + mt) * 8 + gid) * 8 + 4 * (gam >> 1) + hA) = wv;
-                    const float z0 = __uint_as_float(w0 & 0xffff0000u), z1 = __uint_as_float(w1 & 0xffff0000u);
-                    za = dec::ffma2(make_float2(p[mt][0][0], p[mt][0][1]), make_float2(z0, z0), za);
-                    za = dec::ffma2(make_float2(p[mt][1][0], p[mt][1][1]), make_float2(z1, z1), za);
+                    *reinterpret_cast<uint2*>(wst + (gr * 2 + mt) * 64 + (GM == 4 ? 0 : 4 * (gr >> 1))) = wv;
+                    const float2 zz = make_float2(__uint_as_float(w0 & 0xffff0000u), __uint_as_float(w1 & 0xffff0000u));
+                    za0 = dec::ffma2(make_float2(p[mt][0][0], p[mt][1][0]), zz, za0);
+                    za1 = dec::ffma2(make_float2(p[mt][0][1], p[mt][1][1]), zz, za1);
                 }
-                zacc[gr][0] = za.x;
-                zacc[gr][1] = za.y;
+                zacc2[gr][0] = za0;
+                zacc2[gr][1] = za1;
             }
         }
         __syncwarp();
@@ -907,6 +914,11 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
         for (int st = 0; st < Gm::NS; ++st) asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bars + st)));
     }
     // ---- warp epilogue: l over the 8 row-groups, zero sums, o = D * 2^(24 - P(row) - kp) + zacc ----
+    float zacc[4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) zacc[i][j] = zacc2[i][j].x + zacc2[i][j].y;
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
         float l = (GM == 8 || tig < 2) ? l_part[j] : 0.0f;
