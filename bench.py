@@ -283,6 +283,7 @@ def run_kvt(args):
         Vp = torch.randn(B, H, S0, D, device=dev, generator=gen).to(torch.bfloat16)
         kvt.quantize_append(cache, Kp, Vp, len0, nS0, len_before_host=[0] * B, n_new_host=[S0] * B)
         del Kp, Vp
+        torch.cuda.empty_cache()                              # large batches: keep the prefill temporaries from fragmenting HBM
         caches.append(cache)
     torch.cuda.synchronize()
     # ---- per-step inputs (resident): new k, v per layer and q per layer ----

@@ -1,0 +1,2 @@
+mkdir -p gpurun_out
+timeout 2400 python tools/sweep_ctx.py > gpurun_out/sweep.log 2>&1

@@ -1,0 +1,42 @@
+"""BASELINE config 4: uniform KIVI-KV8 vs the searched mixed map (Llama-3.1-8B shape), context sweep 1k-32k,
+batch at the HBM limit (50% of free memory for the cache, leaving room for the prefill temporaries).
+Runs bench.py per point and writes one JSON record per point to gpurun_out/sweep_ctx.jsonl.
+    python tools/sweep_ctx.py [--ctx 1024 2048 ...]"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import torch
+
+ROOT = Path(__file__).resolve().parents[1]
+ap = argparse.ArgumentParser()
+ap.add_argument("--ctx", type=int, nargs="*", default=[1024, 2048, 4096, 8192, 16384, 32768])
+ap.add_argument("--frac", type=float, default=0.5)
+a = ap.parse_args()
+free, _ = torch.cuda.mem_get_info()
+# packed bytes per token per layer-set (all 32 layers x 8 KV heads): 3.25 map 136 B, KV8 288 B per token-head
+per_tok = {"llama-3.25": 136 * 8 * 32, "llama-kv8": 288 * 8 * 32}
+out = ROOT / "gpurun_out" / "sweep_ctx.jsonl"
+out.parent.mkdir(exist_ok=True)
+with open(out, "w") as f:
+    for ctx in a.ctx:
+        for w in ("llama-3.25", "llama-kv8"):
+            B = int(a.frac * free / (per_tok[w] * (ctx + 128)))
+            B = max(8, min(B, 4096)) // 8 * 8
+            r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--workload", w, "--batch", str(B), "--ctx", str(ctx),
+                                "--steps", "20", "--warmup", "3", "--no-e2e", "--no-cpu-baseline"],
+                               capture_output=True, text=True, cwd=ROOT, timeout=1200,
+                               env=dict(os.environ, PYTORCH_CUDA_ALLOC_CONF="expandable_segments:True"))
+            lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+            rec = {"workload": w, "ctx": ctx, "batch": B}
+            if lines:
+                j = json.loads(lines[-1])
+                rec.update(tokens_per_s=j["value"], ms_per_step=j["ms_per_step"], frac=j["roofline"]["frac"],
+                           attn_gbs=j["roofline"]["achieved"], clocks=j["clocks"])
+            else:
+                rec["error"] = r.stderr[-500:]
+            print(json.dumps(rec), flush=True)
+            f.write(json.dumps(rec) + "\n")
