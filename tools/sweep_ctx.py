@@ -1,7 +1,7 @@
-"""BASELINE config 4: uniform KIVI-KV8 vs the searched mixed map (Llama-3.1-8B shape), context sweep 1k-32k,
+"""BASELINE config 4: uniform KIVI-KV8 vs the searched mixed map (Llama-3.1-8B or Qwen2.5-7B shape), context sweep 1k-32k,
 batch at the HBM limit (50% of free memory for the cache, leaving room for the prefill temporaries).
-Runs bench.py per point and writes one JSON record per point to gpurun_out/sweep_ctx.jsonl.
-    python tools/sweep_ctx.py [--ctx 1024 2048 ...]"""
+Runs bench.py per point and writes one JSON record per point to gpurun_out/sweep_ctx_<model>.jsonl.
+    python tools/sweep_ctx.py [--model llama|qwen] [--ctx 1024 2048 ...]"""
 import argparse
 import json
 import os
@@ -15,15 +15,18 @@ ROOT = Path(__file__).resolve().parents[1]
 ap = argparse.ArgumentParser()
 ap.add_argument("--ctx", type=int, nargs="*", default=[1024, 2048, 4096, 8192, 16384, 32768])
 ap.add_argument("--frac", type=float, default=0.5)
+ap.add_argument("--model", default="llama", choices=["llama", "qwen"])
 a = ap.parse_args()
 free, _ = torch.cuda.mem_get_info()
 # packed bytes per token per layer-set (all 32 layers x 8 KV heads): 3.25 map 136 B, KV8 288 B per token-head
-per_tok = {"llama-3.25": 136 * 8 * 32, "llama-kv8": 288 * 8 * 32}
-out = ROOT / "gpurun_out" / "sweep_ctx.jsonl"
+per_tok = {"llama-3.25": 136 * 8 * 32, "llama-kv8": 288 * 8 * 32,      # Llama: 32 layers x 8 KV heads
+           "qwen-4.00": 160 * 4 * 28, "qwen-kv8": 288 * 4 * 28}         # Qwen: 28 layers x 4 KV heads
+pair = ("llama-3.25", "llama-kv8") if a.model == "llama" else ("qwen-4.00", "qwen-kv8")
+out = ROOT / "gpurun_out" / f"sweep_ctx_{a.model}.jsonl"
 out.parent.mkdir(exist_ok=True)
 with open(out, "w") as f:
     for ctx in a.ctx:
-        for w in ("llama-3.25", "llama-kv8"):
+        for w in pair:
             B = int(a.frac * free / (per_tok[w] * (ctx + 128)))
             B = max(8, min(B, 4096)) // 8 * 8
             r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--workload", w, "--batch", str(B), "--ctx", str(ctx),
