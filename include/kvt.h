@@ -158,7 +158,12 @@ int32_t kvt_quantize_append(const kvt_layer_cache* cache, const void* k_new, con
  * softmax_scale is normally 1/sqrt(d) (A9).  A sequence of length 0 yields a zero row.
  * The split-KV partials live in `workspace` (size from kvt_decode_workspace_bytes).  The workspace must
  * be zero-filled before its first use (it holds per-(b, kv head) split-arrival counters); every call
- * leaves those counters at zero again, so one workspace can be reused by consecutive calls on a stream. */
+ * leaves those counters at zero again, so one workspace can be reused by consecutive calls on a stream.
+ * Ordering: tile-record layers launch as a programmatic dependent (PDL) of the preceding kernel in the stream
+ * when the grid (nearly) fills the GPU; before waiting for that kernel they read only q and seq_len_dev, so
+ * those must be complete before the preceding kernel started — always true after kvt_quantize_append (the
+ * only libkvt kernel that lets its dependents start early) and after any kernel that does not trigger them.
+ * The cache, the workspace and the outputs are touched only after the wait. */
 int32_t kvt_decode_workspace_bytes(const kvt_layer_cache* cache, int32_t n_q_heads,
                                    const int32_t* seq_len_host, uint64_t* bytes);
 int32_t kvt_decode_attention(const kvt_layer_cache* cache, const void* q, int32_t n_q_heads,
