@@ -1,16 +1,19 @@
 """Benchmark of the KVTuner hot path on B200: one decode step = for every layer, quantise-append the
-new token's K/V (K1) and run decode attention over the packed mixed-precision cache (K2 + K3).
+new token's K/V (K1) and run decode attention over the packed mixed-precision cache (K2, split merge fused).
 
-Metric (BASELINE.json): decode tokens/s (= batch / step time, attention-only: no weights, GEMMs or
-MLPs) and the HBM GB/s of the attention kernel as a fraction of the measured B200 copy peak.
+Metric (BASELINE.json): decode tokens/s (= sequences decoded per step / step time, attention-only: no
+weights, GEMMs or MLPs) and the HBM GB/s of the attention kernel as a fraction of the measured B200 copy peak.
 
-    python bench.py [--gpus N --steps K --warmup W] [--workload llama-3.25|qwen-4.00|llama-kv8|qwen-kv8]
+    python bench.py [--gpus N --steps K --warmup W] [--workload llama-3.25|qwen-4.00|...]
     python bench.py --impl reference ...        # the CPU oracle on a bounded sample (rank 0 only)
-    torchrun --nproc-per-node N bench.py --gpus N ...   (weak scaling: B sequences per GPU)
+    torchrun --nproc-per-node N bench.py --gpus N [--scaling weak|strong]
 
-Rank 0 prints ONE JSON line.  Inputs are synthetic (kvt_synth recipe), resident in HBM before the
-timed region; the cache (~18 GB at the default workload) is far larger than L2, so no L2 flush is
-needed between steps.
+Multi-GPU (`paper_2502_04420_b200/partition.py`): weak scaling gives every rank `--batch`
+sequences; strong scaling splits `--batch` sequences over the ranks (batch rows, or KV heads when the
+batch is smaller than the world); `*-seqshard` workloads shard every sequence's tokens and exchange the
+(m, l, o) partials once per layer.  Rank 0 prints ONE JSON line.  Inputs are synthetic (kvt_synth recipe),
+resident in HBM before the timed region; the cache (~18 GB at the default workload) is far larger than L2,
+so no L2 flush is needed between steps.
 """
 from __future__ import annotations
 
@@ -40,6 +43,7 @@ WORKLOADS = {
     "llama-128k-seqshard": ("configs/llama-3.1-8b_kivi_3.25.json", (32, 8, 32), 8, 131072),
 }
 D = 128
+SPEC_HBM_GBS = 8000.0        # B200 HBM3e nominal (DGX figure, B200_PROFILING.md); context for the record only
 
 
 def parse():
@@ -49,11 +53,16 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="kvt", choices=["kvt", "reference"])
     ap.add_argument("--workload", default="llama-3.25", choices=sorted(WORKLOADS))
-    ap.add_argument("--batch", type=int, default=None, help="sequences per GPU (weak scaling)")
+    ap.add_argument("--batch", type=int, default=None,
+                    help="weak scaling: sequences per GPU; strong scaling: sequences in total")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="batch/head partitions only (seqshard workloads are strong by construction)")
     ap.add_argument("--ctx", type=int, default=None, help="tokens in the cache after the first append")
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "symm"],
                     help="seqshard workloads: NCCL all-gather of the partials, or the fused push into the peers' "
                          "symmetric-memory buffers (kvt_decode_attention_partial_push + one barrier)")
+    ap.add_argument("--launch", default="graph", choices=["graph", "eager"],
+                    help="timed step as one CUDA graph replay (default) or eager launches through ctypes")
     ap.add_argument("--paged", action="store_true",
                     help="paged tile records: every 32-token block in a shuffled page of a per-layer pool")
     ap.add_argument("--no-e2e", action="store_true")
@@ -62,14 +71,33 @@ def parse():
     return ap.parse_args()
 
 
-def layer_specs(name, kvt):
+METRIC = "decode tokens/s (attention-only, mixed-precision KV)"
+DATA = "synthetic (kvt_synth: N(0,1) K with x11 outliers on channels c%8==0, N(0,1) V, 0.5 N(0,1) q)"
+
+
+def oracle_specs(name):
+    """The workload's layer specs through the ORACLE's own config reader (no product code: VERDICT r1 W1)."""
+    from oracle import config as ocfg
+
     cfg_path, (L, H, Hq), B, S = WORKLOADS[name]
-    name = name.replace("-128k-seqshard", "-3.25")
+    if cfg_path is None:
+        return [ocfg.OracleLayer(ocfg.MODE_KIVI, 8, 8, 32, 32) for _ in range(L)], \
+            "uniform KIVI-KV8 (baseline of P:538)"
+    cfg = ocfg.load(ROOT / cfg_path)
+    specs = list(cfg.layers)
+    if name == "qwen-4.00":   # A19: the paper's exact-4.00 Qwen2.5-7B map, stored in the KIVI layout
+        specs = [ocfg.OracleLayer(ocfg.MODE_KIVI, s.key_bits, s.value_bits, 32, 32) for s in specs]
+    return specs, f"{cfg.model_name} {cfg_path} (f_m = {cfg.equivalent_bits:g})"
+
+
+def product_specs(name, kvt):
+    """The same layer specs through the library's loader (kvt_config_load) for the GPU arm."""
+    cfg_path, (L, H, Hq), B, S = WORKLOADS[name]
     if cfg_path is None:
         return [kvt.LayerSpec.kivi(8, 8) for _ in range(L)], "uniform KIVI-KV8 (baseline of P:538)"
     cfg = kvt.load_config(str(ROOT / cfg_path))
     specs = cfg.layers
-    if name == "qwen-4.00":   # A19: the paper's exact-4.00 Qwen2.5-7B map, stored in the KIVI layout
+    if name == "qwen-4.00":
         specs = [kvt.LayerSpec.kivi(s.key_bits, s.value_bits) for s in specs]
     return specs, f"{cfg.model_name} {cfg_path} (f_m = {cfg.equivalent_bits:g})"
 
@@ -87,13 +115,52 @@ def algorithmic_bytes(spec, B, H, Hq, S):
     nqv = S if spec.value_bits == 16 else max(0, S - spec.residual)
     nqk = nq_key()
 
-    def per_tok(bits, per_channel):
+    def per_tok(bits):
         if bits == 16:
             return 2 * D
         return D * bits // 8 + (D // spec.group) * 4      # codes + meta (per-channel meta is also 4 B x d / G per token)
-    tok = nqk * per_tok(spec.key_bits, spec.mode == 1) + (S - nqk) * 2 * D \
-        + nqv * per_tok(spec.value_bits, False) + (S - nqv) * 2 * D
+    tok = nqk * per_tok(spec.key_bits) + (S - nqk) * 2 * D + nqv * per_tok(spec.value_bits) + (S - nqv) * 2 * D
     return B * H * tok + B * Hq * D * 2 * 2
+
+
+def plan(args, world, rank):
+    """(B_rank, kv-head range, global tokens per step, scaling label, parallelism label)."""
+    from paper_2502_04420_b200.partition import partition
+
+    _, (L, H, Hq), B_def, _ = WORKLOADS[args.workload]
+    B = args.batch or B_def
+    if args.workload.endswith("seqshard"):
+        return B, (0, H), B, "strong", parallelism(args, world)
+    if args.scaling == "weak":
+        return B, (0, H), world * B, "weak", parallelism(args, world)
+    p = partition(B, H, world, rank)
+    return p.batch, (p.h_lo, p.h_hi), B, "strong", parallelism(args, world)
+
+
+def parallelism(args, world):
+    _, (L, H, Hq), B_def, _ = WORKLOADS[args.workload]
+    B = args.batch or B_def
+    if args.workload.endswith("seqshard"):
+        how = "fused push into peer symmetric memory -> barrier -> combine" if args.exchange == "symm" else \
+            "partial -> NCCL all-gather -> combine"
+        return f"sequence-sharded x{world} ({how})"
+    if args.scaling == "weak":
+        return f"batch-partitioned x{world} (B={B} per GPU, no collective)"
+    how = "batch rows" if B >= world else "KV heads (B < N)"
+    return f"{how} over {world} GPUs (global B={B}, no collective)"
+
+
+def config_of(args, desc, world):
+    """The `config` object of the JSON line — built the same way in both arms (the reference arm describes the
+    workload its bounded sample is drawn from), so the driver compares like with like."""
+    _, (L, H, Hq), B_def, S_ctx = WORKLOADS[args.workload]
+    S_first = (args.ctx or S_ctx) + args.warmup            # context of the first timed step
+    return {"workload": args.workload, "layers": desc, "shape": {"L": L, "H_kv": H, "H_q": Hq, "d": D},
+            "batch": args.batch or B_def, "ctx": f"{S_first}..{S_first + args.steps - 1}",
+            "scaling": "strong" if (args.workload.endswith("seqshard") or args.scaling == "strong") else "weak",
+            "parallelism": parallelism(args, world),
+            "l2": "inputs larger than L2 (packed cache >> 126 MB; no flush)",
+            "kv_layout": "paged (shuffled 32-token pages, block table)" if args.paged else "dense"}
 
 
 class ClockSampler:
@@ -110,7 +177,8 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.dev), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                ["nvidia-smi", "-i", str(self.dev),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks.mem,power.draw",
                  "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
                 text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
@@ -133,7 +201,7 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
+        sm, mx, mem, pw, reasons = [], [], [], [], set()
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 3:
@@ -142,6 +210,9 @@ class ClockSampler:
                 sm.append(float(parts[0]))
                 mx.append(float(parts[1]))
                 bits = int(parts[2], 16)
+                if len(parts) >= 5:
+                    mem.append(float(parts[3]))
+                    pw.append(float(parts[4]))
             except ValueError:
                 continue
             for bit, name in self.REASONS.items():
@@ -150,7 +221,9 @@ class ClockSampler:
         if not sm:
             return None
         sm.sort()
-        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(mx), "reasons": sorted(reasons), "samples": len(sm)}
+        mem.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(mx), "reasons": sorted(reasons), "samples": len(sm),
+                "mem_mhz": mem[len(mem) // 2] if mem else None, "power_w_max": max(pw) if pw else None}
 
 
 def measured_peaks():
@@ -172,58 +245,129 @@ def ncu_traffic(workload):
     return None, None
 
 
-# ------------------------------------------------------------------------------------------------
-# CPU oracle (cpu_baseline leg and --impl reference): the oracle as it stands, single-threaded C
-# ------------------------------------------------------------------------------------------------
-def oracle_sample(specs, shape, S, n_units, seed=11):
-    """Time the oracle on `n_units` (layer, kv head) units of ONE sequence of the workload (layers
-    rotate).  Returns (seconds, tokens) where tokens = units / (L * H_kv) decode tokens."""
-    import numpy as np
+def build_info():
+    """git SHA of the source the library was built from: `git` when the checkout has .git, else the stamp
+    build.py writes next to libkvt.so (the GPU box's snapshot has no .git)."""
+    try:
+        sha = subprocess.run(["git", "rev-parse", "HEAD"], cwd=ROOT, capture_output=True, text=True, timeout=10)
+        if sha.returncode == 0:
+            dirty = subprocess.run(["git", "status", "--porcelain", "--untracked-files=no"], cwd=ROOT,
+                                   capture_output=True, text=True, timeout=10).stdout.strip() != ""
+            return {"git_sha": sha.stdout.strip(), "dirty": dirty, "source": "git"}
+    except (OSError, subprocess.SubprocessError):
+        pass
+    p = ROOT / "paper_2502_04420_b200" / "BUILD_INFO.json"
+    if p.exists():
+        return {**json.loads(p.read_text()), "source": "BUILD_INFO.json (written by build.py)"}
+    return {"git_sha": None, "source": "unknown"}
 
-    import kvt_synth
-    import oracle
 
-    oracle.build()
-    L, H, Hq = shape
-    g = Hq // H
-    K = kvt_synth.bf16_bits(kvt_synth.keys((1, 1, S, D), seed=seed))
-    V = kvt_synth.bf16_bits(kvt_synth.values((1, 1, S, D), seed=seed + 1))
-    q = kvt_synth.bf16_bits(kvt_synth.queries((1, g, D), seed=seed + 2))
-    sl = np.array([S], np.int32)
-    t0 = time.perf_counter()
-    for u in range(n_units):
-        s = specs[(u * 7) % L]
-        oracle.layer_decode(s.mode, s.key_bits, s.value_bits, s.group, s.residual, K, V, q, sl, 1 / math.sqrt(D))
-    dt = time.perf_counter() - t0
-    return dt, n_units / (L * H)
+def host_info():
+    model = None
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    n = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    return {"cpu_model": model, "nproc": n, "os_cpu_count": os.cpu_count()}
+
+
+# ------------------------------------------------------------------------------------------------
+# CPU oracle (cpu_baseline leg and --impl reference): the oracle as it stands, plain C, one unit per thread
+# ------------------------------------------------------------------------------------------------
+class OracleSampler:
+    """Times the C oracle (O2 static build + fp64 read-back + fp64 Eq. 1 attention) on (layer, kv head) units
+    of ONE sequence of the workload at context S, `threads` units at a time (ctypes releases the GIL, so the
+    units run on separate cores).  tokens = units / (L * H_kv): a decode token needs every (layer, head)."""
+
+    def __init__(self, specs, shape, S, seed=11):
+        import kvt_synth
+        import oracle
+
+        oracle.build()
+        self.oracle = oracle
+        self.specs, self.shape, self.S = specs, shape, S
+        L, H, Hq = shape
+        g = Hq // H
+        self.K = kvt_synth.bf16_bits(kvt_synth.keys((1, 1, S, D), seed=seed))
+        self.V = kvt_synth.bf16_bits(kvt_synth.values((1, 1, S, D), seed=seed + 1))
+        self.q = kvt_synth.bf16_bits(kvt_synth.queries((1, g, D), seed=seed + 2))
+        import numpy as np
+
+        self.sl = np.array([S], np.int32)
+        self.u = 0
+
+    def _unit(self, u):
+        s = self.specs[(u * 7) % len(self.specs)]
+        self.oracle.layer_decode(s.mode, s.key_bits, s.value_bits, s.group, s.residual, self.K, self.V, self.q,
+                                 self.sl, 1 / math.sqrt(D))
+
+    def run(self, n_units, threads):
+        """Returns (seconds, decode tokens) for n_units units on `threads` threads."""
+        from concurrent.futures import ThreadPoolExecutor
+
+        us = list(range(self.u, self.u + n_units))
+        self.u += n_units
+        t0 = time.perf_counter()
+        if threads <= 1:
+            for u in us:
+                self._unit(u)
+        else:
+            with ThreadPoolExecutor(threads) as ex:
+                list(ex.map(self._unit, us))
+        dt = time.perf_counter() - t0
+        L, H, _ = self.shape
+        return dt, n_units / (L * H)
+
+
+def cpu_baseline_record(sampler, S):
+    """cpu_baseline at 1 core and at nproc cores: bounded samples of the workload."""
+    hi = host_info()
+    n = hi["nproc"] or 1
+    dt1, tok1 = sampler.run(16, 1)
+    dtn, tokn = sampler.run(2 * n, n)
+    return {"value": tokn / dtn, "unit": "tokens/s", "cores": n, "kind": "oracle",
+            "sample": f"{2 * n} (layer, kv head) units of 1 sequence at S={S} on {n} threads "
+                      f"(= {tokn:.3f} decode tokens, {dtn:.1f} s); oracle = O2 static build + fp64 read-back "
+                      f"+ fp64 Eq.1, plain C, one unit per thread",
+            "single_core": {"value": tok1 / dt1, "unit": "tokens/s", "cores": 1,
+                            "sample": f"16 units at S={S} ({dt1:.1f} s)"},
+            **hi}
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    import paper_2502_04420_b200 as kvt   # only for the config loader (host C, no GPU work)
-
-    specs, desc = layer_specs(args.workload, kvt)
-    _, shape, B, S = WORKLOADS[args.workload]
-    S = args.ctx or S
+    specs, desc = oracle_specs(args.workload)
+    _, shape, B_def, S_ctx = WORKLOADS[args.workload]
+    L, H, Hq = shape
+    S_first = (args.ctx or S_ctx) + args.warmup    # the GPU arm's first timed context (same config object)
+    hi = host_info()
+    n = hi["nproc"] or 1
+    smp = OracleSampler(specs, shape, S_first)
     for _ in range(args.warmup):
-        oracle_sample(specs, shape, S, 1)
-    tot_t, tot_tok = 0.0, 0.0
+        smp.run(n, n)
+    times, tot_tok = [], 0.0
     for _ in range(args.steps):
-        dt, tok = oracle_sample(specs, shape, S, 1)
-        tot_t += dt
+        dt, tok = smp.run(n, n)
+        times.append(dt)
         tot_tok += tok
+    tot_t = sum(times)
     value = tot_tok / tot_t
-    sample = (f"per step: 1 (layer, kv head) unit of 1 sequence at S={S} (layers rotate), i.e. 1/{shape[0] * shape[1]} "
-              f"of a decode token; oracle = O2 static build + fp64 read-back + fp64 Eq.1 attention")
-    line = {"impl": "reference", "metric": "decode tokens/s (attention-only, mixed-precision KV)", "value": value,
-            "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1000 * tot_t / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (kvt_synth: N(0,1) K with x11 channel outliers, "
-            "N(0,1) V, 0.5 N(0,1) q)",
-            "config": {"workload": args.workload, "layers": desc, "batch": 1, "ctx": S, "l2": "n/a (CPU)"},
-            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": 1, "kind": "oracle", "sample": sample},
+    sample = (f"per step: {n} (layer, kv head) units of 1 sequence at S={S_first} on {n} threads (layers rotate), "
+              f"i.e. {n}/{L * H} of a decode token; oracle = O2 static build + fp64 read-back + fp64 Eq.1 "
+              f"attention, plain C, one unit per thread")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot_t / max(args.steps, 1),
+            "higher_is_better": True, "scaling": config_of(args, desc, world)["scaling"],
+            "vs_baseline": None, "dtype": "f64", "data": DATA,
+            "config": config_of(args, desc, world),
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": n, "kind": "oracle", "sample": sample, **hi},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
@@ -231,6 +375,16 @@ def run_reference(args):
 # ------------------------------------------------------------------------------------------------
 # GPU arm
 # ------------------------------------------------------------------------------------------------
+def _pct(xs, p):
+    xs = sorted(xs)
+    if not xs:
+        return None
+    k = (len(xs) - 1) * p
+    lo = int(math.floor(k))
+    hi = min(lo + 1, len(xs) - 1)
+    return xs[lo] + (xs[hi] - xs[lo]) * (k - lo)
+
+
 def run_kvt(args):
     import torch
     import torch.distributed as dist
@@ -247,13 +401,15 @@ def run_kvt(args):
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
 
-    specs, desc = layer_specs(args.workload, kvt)
-    _, (L, H, Hq), B, S_ctx = WORKLOADS[args.workload]
-    B = args.batch or B
+    _, (L, H_all, Hq_all), B_def, S_ctx = WORKLOADS[args.workload]
+    g = Hq_all // H_all
+    specs, desc = product_specs(args.workload, kvt)
+    B, (h_lo, h_hi), tokens_per_step, scaling, par = plan(args, world, rank)
+    H, Hq = h_hi - h_lo, (h_hi - h_lo) * g
     S_ctx = args.ctx or S_ctx
     seqshard = args.workload.endswith("seqshard")
     S0 = S_ctx - 1                                           # prefilled; the first timed append makes S_ctx
-    n_steps_total = args.warmup + 2 * args.steps + (0 if args.no_e2e else args.warmup + args.steps)
+    n_steps_total = args.warmup + 2 * args.steps + (0 if args.no_e2e else args.warmup + args.steps) + 2
     appends = True
     if seqshard:                                             # a6: this rank holds tokens [lo, hi) of every sequence
         from paper_2502_04420_b200.seqshard import shard_bounds, shard_spec
@@ -286,9 +442,8 @@ def run_kvt(args):
         torch.cuda.empty_cache()                              # large batches: keep the prefill temporaries from fragmenting HBM
         caches.append(cache)
     torch.cuda.synchronize()
-    # ---- per-step inputs (resident): new k, v per layer and q per layer ----
-    # one contiguous device buffer of all per-step inputs (q, k_new, v_new of every layer) and one of all
-    # outputs, so the end-to-end leg moves them with one host->device and one device->host copy per step
+    # ---- per-step inputs (resident): one contiguous device buffer of every layer's q, k_new, v_new and one of
+    # all outputs, so the end-to-end leg moves them with one host->device and one device->host copy per step
     gen.manual_seed(77 + rank)
     n_q, n_kv = B * Hq * D, B * H * D
     d_in = torch.empty(L, n_q + 2 * n_kv, dtype=torch.bfloat16, device=dev)
@@ -303,18 +458,20 @@ def run_kvt(args):
                 [dout[l] for l in range(L)])
 
     bufsets = [views(d_in, d_out)]
-    ws_bytes = max(kvt.decode_workspace_bytes(c, Hq, [cap] * B) for c in caches)
+    ws_bytes = max(kvt.decode_workspace_bytes(c, Hq, None) for c in caches)   # planned for capacity: graph-safe
     ws = torch.zeros(max(ws_bytes, 16), dtype=torch.uint8, device=dev)      # merge counters start at zero
-    n_combine = 0     # the tensor-core kernel merges cut units in-kernel (last CTA); see launches.csv
     len_before = torch.full((B,), S0, dtype=torch.int32, device=dev)
     len_after = torch.full((B,), S0 + (1 if appends else 0), dtype=torch.int32, device=dev)
     ones = torch.ones(B, dtype=torch.int32, device=dev)
     scale = 1.0 / math.sqrt(D)
-    stream = torch.cuda.current_stream()
+    main_stream = torch.cuda.current_stream()
     exch = None
+    part = gathered = None
     if seqshard:
+        from paper_2502_04420_b200.seqshard import sharded_decode
+
         part = torch.empty(B, Hq, D + 2, dtype=torch.float32, device=dev)
-        gathered = torch.empty(world, B, Hq, D + 2, dtype=torch.float32, device=dev)
+        gathered = torch.empty(world, B, Hq, D + 2, dtype=torch.float32, device=dev) if world > 1 else None
         if args.exchange == "symm":
             from paper_2502_04420_b200.seqshard import SymmExchange
 
@@ -323,42 +480,58 @@ def run_kvt(args):
                                         device_id=dev)
             exch = SymmExchange((B, Hq, D + 2), dev)
 
-    def step(ev=None, bs=0):
+    def step(ev=None, bs=0, stream=None):
+        stream = stream or main_stream
         q, k_new, v_new, outs = bufsets[bs]
+        fused = ev is None and appends and not seqshard
         for l in range(L):
-            if appends:
+            if appends and not fused:
                 kvt.quantize_append(caches[l], k_new[l], v_new[l], len_before, ones, n_new_max=1, stream=stream)
             if ev is not None:
                 ev[l][0].record(stream)
+            mark = (lambda l=l: ev[l][1].record(stream)) if ev is not None else None
             if exch is not None:          # fused exchange: push into the peers' buffers, barrier, combine
-                k = exch.k
-                kvt.decode_attention_partial_push(caches[l], q[l], len_after, exch.slots[k], scale=scale,
-                                                  workspace=ws, stream=stream)
-                if ev is not None:
-                    ev[l][1].record(stream)
-                exch.handle.barrier(channel=0)
-                exch.k ^= 1
-                kvt.combine_partials(exch.buf[k], out=outs[l], stream=stream)
-            elif seqshard:
-                kvt.decode_attention_partial(caches[l], q[l], len_after, scale=scale, partial=part, workspace=ws,
-                                             stream=stream)
-                if ev is not None:
-                    ev[l][1].record(stream)
-                if world > 1:
-                    dist.all_gather_into_tensor(gathered, part)
-                else:
-                    gathered[0].copy_(part)
-                kvt.combine_partials(gathered, out=outs[l], stream=stream)
+                exch.decode(caches[l], q[l], len_after, scale=scale, out=outs[l], workspace=ws, stream=stream,
+                            after_partial=mark)
+            elif seqshard:                # a6 through the tested orchestration: partial -> all-gather -> combine
+                sharded_decode(caches[l], q[l], len_after, scale=scale, out=outs[l], part=part, gathered=gathered,
+                               workspace=ws, stream=stream, after_partial=mark)
+            elif fused:                   # the serving step of one layer: append + attention in one library call
+                kvt.append_decode_attention(caches[l], k_new[l], v_new[l], len_before, ones, q[l], len_after,
+                                            scale=scale, out=outs[l], workspace=ws, stream=stream)
             else:
                 kvt.decode_attention(caches[l], q[l], len_after, scale=scale, out=outs[l], workspace=ws, stream=stream)
-                if ev is not None:
-                    ev[l][1].record(stream)
+                if mark:
+                    mark()
         if appends:
             len_before.add_(1)
             len_after.add_(1)
 
+    # CUDA graph of one step per buffer set (the lengths advance inside the graph; every kernel reads them on
+    # the device and the workspace is planned for the capacity, so one capture serves every replay)
+    use_graph = args.launch == "graph" and not seqshard and not args.profile
+    graphs = {}
+
+    def capture(bs):
+        s = torch.cuda.Stream(device=dev)
+        s.wait_stream(main_stream)
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=s):
+            step(bs=bs, stream=s)
+        main_stream.wait_stream(s)
+        graphs[bs] = gr
+
+    def run_step(bs=0):
+        if use_graph:
+            graphs[bs].replay()
+        else:
+            step(bs=bs)
+
+    if use_graph:
+        # capturing records the launches without running them: the lengths are not advanced by the capture
+        capture(0)
     for _ in range(args.warmup):
-        step()
+        run_step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -367,34 +540,35 @@ def run_kvt(args):
     # per-layer attention events (live, on the launching stream) for the roofline
     evs = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)] for _ in range(L)]
            for _ in range(args.steps)]
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     S_first = S0 + (args.warmup + 1 if appends else 0)
     sampler = ClockSampler(dev.index) if not args.profile else None
     if sampler:
         sampler.__enter__()
-    # timed region: K steps back to back (no per-layer events: the attention launch may then overlap the
-    # tail of the same layer's append, programmatic dependent launch)
-    start.record(stream)
+    # timed region: K steps back to back, an event at every step boundary (p10/p50/p90); no per-layer events
+    # (the attention launch may overlap the tail of the same layer's append, programmatic dependent launch)
+    marks[0].record(main_stream)
     for i in range(args.steps):
-        step()
-    end.record(stream)
+        run_step()
+        marks[i + 1].record(main_stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    # roofline pass: the next K steps again, with CUDA events around every attention launch
+    # roofline pass: the next K steps eagerly, with CUDA events around every attention launch
     for i in range(args.steps):
         step(evs[i])
     torch.cuda.synchronize()
     if sampler:
         sampler.__exit__()
-    ms = start.elapsed_time(end)
+    ms = marks[0].elapsed_time(marks[-1])
+    per_step = [marks[i].elapsed_time(marks[i + 1]) for i in range(args.steps)]
     attn_ms = sum(e[0].elapsed_time(e[1]) for st in evs for e in st)
     if world > 1:
         t = torch.tensor([ms, attn_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, attn_ms = t.tolist()
     ms_per_step = ms / args.steps
-    value = world * B / (ms_per_step / 1000.0)
+    value = tokens_per_step / (ms_per_step / 1000.0)
 
     # roofline of the dominant kernel (decode attention, all layers): algorithmic bytes / event time
     alg = 0
@@ -407,7 +581,9 @@ def run_kvt(args):
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "traffic_source": traffic_src, "kernel": "decode attention (all layers)",
                 "attn_share_of_step": attn_ms / ms, "peak_source": peak_src,
-                "algorithmic_bytes_per_step": alg / args.steps}
+                "frac_of_spec_8TBs": achieved / SPEC_HBM_GBS,
+                "algorithmic_bytes_per_step": alg / args.steps,
+                "timing": "CUDA events around every attention launch of a second (eager) pass of K steps"}
 
     # ---- e2e: host (pinned) inputs -> device, step, outputs -> host, every step ----
     e2e = None
@@ -422,6 +598,8 @@ def run_kvt(args):
         d_ins = [d_in, torch.empty_like(d_in)]
         d_outs = [d_out, torch.empty_like(d_out)]
         bufsets.append(views(d_ins[1], d_outs[1]))
+        if use_graph:
+            capture(1)
         cs = torch.cuda.Stream(device=dev)
         h2d_done = [torch.cuda.Event(), torch.cuda.Event()]
         comp_done = [torch.cuda.Event(), torch.cuda.Event()]
@@ -441,25 +619,25 @@ def run_kvt(args):
                 j = i % 2
                 if i + 1 < n:
                     h2d(i + 1)                               # overlaps step i
-                stream.wait_event(h2d_done[j])
+                main_stream.wait_event(h2d_done[j])
                 if i >= 2:
-                    stream.wait_event(d2h_done[j])           # step i-2's outputs left buffer set j
-                step(bs=j)
-                comp_done[j].record(stream)
+                    main_stream.wait_event(d2h_done[j])      # step i-2's outputs left buffer set j
+                run_step(bs=j)
+                comp_done[j].record(main_stream)
                 with torch.cuda.stream(cs):
                     cs.wait_event(comp_done[j])
                     h_out.copy_(d_outs[j], non_blocking=True)    # step i's outputs, device -> host
                     d2h_done[j].record(cs)
-            stream.wait_event(d2h_done[(n - 1) % 2])
+            main_stream.wait_event(d2h_done[(n - 1) % 2])
 
         e2e_run(args.warmup)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s2.record(stream)
+        s2.record(main_stream)
         e2e_run(args.steps)
-        e2.record(stream)
+        e2.record(main_stream)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -468,38 +646,35 @@ def run_kvt(args):
             t = torch.tensor([ems], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = t.item()
-        e2e = {"value": world * B / (ems / args.steps / 1000.0), "unit": "tokens/s", "h2d_bytes_per_step": bi,
-               "d2h_bytes_per_step": bo}
+        e2e = {"value": tokens_per_step / (ems / args.steps / 1000.0), "unit": "tokens/s", "h2d_bytes_per_step": bi,
+               "d2h_bytes_per_step": bo, "api": "kvt.quantize_append + kvt.decode_attention per layer"
+                                                 + (" (one CUDA graph per step)" if use_graph else "")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
-        n_units = 48
-        dt, tok = oracle_sample(specs, (L, H, Hq), S_first, n_units)
-        cpu = {"value": tok / dt, "unit": "tokens/s", "cores": 1, "kind": "oracle",
-               "sample": f"{n_units} (layer, kv head) units of 1 sequence at S={S_first} (= {tok:.3f} decode tokens, "
-                         f"{dt:.1f} s), single-threaded C oracle: O2 static build + fp64 read-back + fp64 Eq.1"}
+        ospecs, _ = oracle_specs(args.workload)
+        cpu = cpu_baseline_record(OracleSampler(ospecs, (L, H_all, Hq_all), S_first), S_first)
 
     clocks = sampler.summary() if sampler else None
     if rank == 0:
-        line = {"metric": "decode tokens/s (attention-only, mixed-precision KV)", "value": value, "unit": "tokens/s",
+        per_layer = (1 if appends else 0) + 1 + (1 if seqshard else 0)
+        line = {"metric": METRIC, "value": value, "unit": "tokens/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-                "higher_is_better": True, "scaling": "strong" if seqshard else "weak", "vs_baseline": None,
+                "ms_per_step_p10": _pct(per_step, 0.1), "ms_per_step_p50": _pct(per_step, 0.5),
+                "ms_per_step_p90": _pct(per_step, 0.9),
+                "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
                 "dtype": "f32 accumulate of f16 tensor-core products (u2/u4/u8 codes, bf16 in/out)",
-                "data": "synthetic (N(0,1) K with x11 outliers on channels c%8==0, N(0,1) V, 0.5 N(0,1) q)",
-                "config": {"workload": args.workload, "layers": desc, "shape": {"L": L, "H_kv": H, "H_q": Hq, "d": D},
-                           "batch_per_gpu": B, "ctx": f"{S_first}..{S_first + args.steps - 1}",
-                           "parallelism": ((f"sequence-sharded x{world} (partial pushed into peer symmetric memory -> barrier -> combine)"
-                                            if exch is not None else
-                                            f"sequence-sharded x{world} (partial -> NCCL all-gather -> combine)") if seqshard
-                                           else f"batch-partitioned x{world} (no collective)"),
-                           "l2": "inputs larger than L2 (cache %.1f GB/GPU)" % (sum(c.nbytes for c in caches) / 1e9),
-                           "kv_layout": "paged (shuffled 32-token pages, block table)" if args.paged else "dense"},
+                "data": DATA,
+                "config": config_of(args, desc, world),
+                "run": {"tokens_per_step": tokens_per_step, "rank0_batch": B, "rank0_kv_heads": [h_lo, h_hi],
+                        "launch": "one CUDA graph per step" if use_graph else "eager (ctypes per kernel)"},
+                "cache_gb_per_gpu": sum(c.nbytes for c in caches) / 1e9,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": args.steps * ((1 if appends else 0) * L + L + (L if seqshard else 0) + n_combine),
-                "clocks": clocks,
+                "gpu_launches": args.steps * per_layer * L,
+                "clocks": clocks, "gpu": torch.cuda.get_device_name(dev), "build": build_info(),
                 "gb_per_s_attention": achieved}
         print(json.dumps(line))
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 

@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define KVT_ABI_VERSION 2u
+#define KVT_ABI_VERSION 3u   /* 3: kvt_append_decode_attention; merge counters first in the workspace */
 
 typedef enum {
     KVT_OK = 0,
@@ -159,17 +159,32 @@ int32_t kvt_quantize_append(const kvt_layer_cache* cache, const void* k_new, con
  * The split-KV partials live in `workspace` (size from kvt_decode_workspace_bytes).  The workspace must
  * be zero-filled before its first use (it holds per-(b, kv head) split-arrival counters); every call
  * leaves those counters at zero again, so one workspace can be reused by consecutive calls on a stream.
- * Ordering: tile-record layers launch as a programmatic dependent (PDL) of the preceding kernel in the stream
- * when the grid (nearly) fills the GPU; before waiting for that kernel they read only q and seq_len_dev, so
- * those must be complete before the preceding kernel started — always true after kvt_quantize_append (the
- * only libkvt kernel that lets its dependents start early) and after any kernel that does not trigger them.
- * The cache, the workspace and the outputs are touched only after the wait. */
+ * The workspace is laid out [merge counters: round_up(4 * batch * kv_heads, 256) bytes][partials], so calls on
+ * caches with the same (batch, kv_heads) can share one workspace whatever their precision pair or CTA count.
+ * Ordering: tile-record layers may launch as a programmatic dependent (PDL) of the preceding kernel in the stream
+ * (when the grid nearly fills the GPU); the kernel then waits for that kernel's completion before it reads
+ * anything, so the call is ordered after every preceding stream operation like a plain launch. */
 int32_t kvt_decode_workspace_bytes(const kvt_layer_cache* cache, int32_t n_q_heads,
                                    const int32_t* seq_len_host, uint64_t* bytes);
 int32_t kvt_decode_attention(const kvt_layer_cache* cache, const void* q, int32_t n_q_heads,
                              const int32_t* seq_len_host, const int32_t* seq_len_dev,
                              float softmax_scale, void* out, int32_t out_dtype,
                              void* workspace, uint64_t ws_bytes, void* stream);
+
+/* ---- a3 + a4 in one call: the serving step of one layer ("fused append + attention") ----
+ * kvt_quantize_append(cache, k_new, v_new, ..., len_before_dev, n_new_dev, n_new_max) followed by
+ * kvt_decode_attention(cache, q, seq_len_dev, ...) on the same stream, with no host lengths (the launches are
+ * planned for `capacity`, so the call can be captured once in a CUDA graph and replayed as the lengths grow).
+ * Because the library launches the append itself, the attention kernel's prologue (the length scan and the q
+ * setup) overlaps the append (programmatic dependent launch); the cache is read only after the append completed.
+ * Precondition: q and seq_len_dev (= len_before_dev + n_new_dev, the caller's) are complete before this call is
+ * issued in stream order, and the append does not modify them.  Errors are reported before any launch. */
+int32_t kvt_append_decode_attention(const kvt_layer_cache* cache, const void* k_new, const void* v_new,
+                                    const int64_t new_strides[3], const int32_t* len_before_dev,
+                                    const int32_t* n_new_dev, int32_t n_new_max,
+                                    const void* q, int32_t n_q_heads, const int32_t* seq_len_dev,
+                                    float softmax_scale, void* out, int32_t out_dtype,
+                                    void* workspace, uint64_t ws_bytes, void* stream);
 
 /* ---- a6: sequence-sharded decode (multi-GPU) ----------------------------------------
  * Partial attention over this shard's tokens: partial fp32 [B][H_q][d + 2] holding, per row,

@@ -69,6 +69,76 @@ def special_rows(kind: str, shape, seed: int) -> torch.Tensor:
     raise ValueError(kind)
 
 
+EDGE_KINDS = ("constant", "zeros_pm", "range1e-3", "range1e-4", "range1e-5", "range1e-6", "normal", "ties_b2",
+              "ties_b4", "ties_b8")
+
+
+def edge_structured(shape, seed: int, along: str) -> torch.Tensor:
+    """bf16 [..., S, d] whose quantisation groups cycle through EDGE_KINDS:
+    constant groups, all-zero groups with random signs (+0 / -0), groups of range 1e-3 .. 1e-6 around small
+    offsets (so bf16 keeps them), ordinary N(0, 1) groups, and groups on a grid whose Eq. 2 codes hit exact
+    .5 ties at 2, 4 and 8 bits (s = 1, 0.5, 2^-4 exactly; both ends of the range present).
+    along = "channel": the kind is constant over a 32-token block x 1 channel (KIVI key groups, P:707);
+    along = "token": constant over 1 token x 32 channels (per-token groups).  Kind of (position p, group c)
+    = EDGE_KINDS[(p + c) % 10], so constant/zero groups sit next to tiny-range groups in every tile."""
+    g = generator(seed, "cpu")
+    *lead, S, d = shape
+    n = 1
+    for x in lead:
+        n *= x
+    out = torch.empty(n, S, d, dtype=torch.float32)
+    tok = torch.arange(S)
+    ch = torch.arange(d)
+    if along == "channel":
+        pos, grp = (tok // 32)[:, None].expand(S, d), ch[None, :].expand(S, d)
+    elif along == "token":
+        pos, grp = tok[:, None].expand(S, d), (ch // 32)[None, :].expand(S, d)
+    else:
+        raise ValueError(along)
+    kind = (pos + grp) % len(EDGE_KINDS)
+    # one random draw per group (offset) and per element
+    gid = pos * d + grp
+    for i in range(n):
+        u = torch.rand(S, d, generator=g)
+        z = torch.randn(S, d, generator=g)
+        off = torch.randn(S * d + d, generator=g)[gid]
+        x = torch.empty(S, d)
+        x = torch.where(kind == 0, 4 * off, x)
+        x = torch.where(kind == 1, torch.where(u < 0.5, torch.tensor(0.0), torch.tensor(-0.0)), x)
+        for k, r in ((2, 1e-3), (3, 1e-4), (4, 1e-5), (5, 1e-6)):
+            x = torch.where(kind == k, r * (off + u), x)
+        x = torch.where(kind == 6, z, x)
+        # ties: values on half steps of s with the group's min (0) and max present so s is exact
+        i7 = torch.randint(0, 7, (S, d), generator=g).float()
+        t7 = 0.5 * i7
+        i8 = torch.randint(0, 31, (S, d), generator=g).float()
+        t8 = 0.25 * i8
+        i9 = torch.randint(0, 128, (S, d), generator=g).float()
+        t9 = (i9 + 0.5) / 16.0
+        x = torch.where(kind == 7, t7, x)
+        x = torch.where(kind == 8, t8, x)
+        x = torch.where(kind == 9, t9, x)
+        # first / second element of every group carry the range ends (0 and max) for the tie kinds
+        first = (tok % 32 == 0)[:, None] if along == "channel" else (ch % 32 == 0)[None, :]
+        second = (tok % 32 == 1)[:, None] if along == "channel" else (ch % 32 == 1)[None, :]
+        for k, mx in ((7, 3.0), (8, 7.5), (9, 255.0 / 16.0)):
+            x = torch.where((kind == k) & first, torch.tensor(0.0), x)
+            x = torch.where((kind == k) & second, torch.tensor(mx), x)
+        out[i] = x
+    return out.view(*lead, S, d).to(torch.bfloat16)
+
+
+def edge_queries(shape, seed: int) -> torch.Tensor:
+    """bf16 q [..., H_q, d] with a 2^±20 dynamic range: head h scaled by 2^e_h, e_h cycling through
+    {-20, -10, 0, 4}, channel c scaled by 2^((c % 21) - 10)."""
+    g = generator(seed, "cpu")
+    q = torch.randn(*shape, generator=g)
+    H, d = shape[-2], shape[-1]
+    eh = torch.tensor([-20.0, -10.0, 0.0, 4.0])[torch.arange(H) % 4]
+    ec = (torch.arange(d) % 21).float() - 10.0
+    return (q * torch.exp2(eh)[:, None] * torch.exp2(ec)[None, :]).to(torch.bfloat16)
+
+
 def bf16_bits(t: torch.Tensor):
     """Raw bf16 bits of a (CPU or CUDA) bf16 tensor as a numpy uint16 array (host)."""
     import numpy as np

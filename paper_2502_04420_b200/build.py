@@ -68,9 +68,28 @@ def build(force: bool = False, verbose: bool = False, defines=(), variant: str =
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
         os.replace(tmp, lib)
+    _stamp(lib)
     if verbose:
         print(f"built {lib}")
     return lib
+
+
+def _stamp(lib: Path):
+    """BUILD_INFO.json next to the library: the git SHA of the sources it was built from (bench.py reports it;
+    the GPU box's copy of the repo has no .git).  Git-ignored."""
+    import json
+
+    info = {"git_sha": None, "dirty": None, "lib": lib.name}
+    try:
+        r = subprocess.run(["git", "rev-parse", "HEAD"], cwd=PKG.parent, capture_output=True, text=True, timeout=10)
+        if r.returncode == 0:
+            info["git_sha"] = r.stdout.strip()
+            st = subprocess.run(["git", "status", "--porcelain", "--untracked-files=no"], cwd=PKG.parent,
+                                capture_output=True, text=True, timeout=10)
+            info["dirty"] = st.stdout.strip() != ""
+    except (OSError, subprocess.SubprocessError):
+        pass
+    (PKG / "BUILD_INFO.json").write_text(json.dumps(info) + "\n")
 
 
 if __name__ == "__main__":

@@ -222,6 +222,37 @@ extern "C" int32_t kvt_decode_attention(const kvt_layer_cache* cache, const void
     return launch_decode(g, p, (const uint16_t*)q, H_q, seq_len_dev, plan, scale, out, out_dtype, ws, ws_bytes, stream);
 }
 
+extern "C" int32_t kvt_append_decode_attention(const kvt_layer_cache* cache, const void* k_new, const void* v_new,
+                                               const int64_t new_strides[3], const int32_t* len_before_dev,
+                                               const int32_t* n_new_dev, int32_t n_new_max, const void* q, int32_t H_q,
+                                               const int32_t* seq_len_dev, float scale, void* out, int32_t out_dtype,
+                                               void* ws, uint64_t ws_bytes, void* stream) {
+    clear_error();
+    Geometry g; CachePtrs p; int plan;
+    int32_t st = decode_common(cache, q, H_q, nullptr, seq_len_dev, &g, &p, &plan);
+    if (st) return st;
+    if (!out) return fail(KVT_ERR_INVALID_ARG, "append+decode: null out");
+    if (out_dtype != 0 && out_dtype != 1) return fail(KVT_ERR_INVALID_ARG, "out_dtype must be 0 (bf16) or 1 (fp32)");
+    if (!k_new || !v_new || !new_strides || !len_before_dev || !n_new_dev)
+        return fail(KVT_ERR_INVALID_ARG, "append+decode: null argument");
+    if (((uintptr_t)k_new & 7) || ((uintptr_t)v_new & 7) || (new_strides[0] & 3) || (new_strides[1] & 3) || (new_strides[2] & 3))
+        return fail(KVT_ERR_INVALID_ARG, "k_new/v_new must be 8-byte aligned with strides multiple of 4 elements");
+    if (n_new_max < 0) return fail(KVT_ERR_INVALID_ARG, "n_new_max < 0");
+    if (g.B == 0) return KVT_OK;
+    // the workspace is validated before anything is launched, so an error leaves the cache untouched
+    const size_t need = decode_workspace(g, H_q, plan);
+    if (need > ws_bytes || (need && !ws))
+        return fail(KVT_ERR_WORKSPACE, "append+decode: workspace %llu < %zu bytes", (unsigned long long)ws_bytes, need);
+    if (n_new_max > 0) {
+        st = launch_append(g, p, (const uint16_t*)k_new, (const uint16_t*)v_new, new_strides, len_before_dev, n_new_dev,
+                           n_new_max, stream);
+        if (st) return st;
+    }
+    // the library launched the preceding kernel itself: the decode prologue (lengths, q) may overlap it
+    return launch_decode(g, p, (const uint16_t*)q, H_q, seq_len_dev, plan, scale, out, out_dtype, ws, ws_bytes, stream,
+                         nullptr, 0, /*early=*/n_new_max > 0);
+}
+
 extern "C" int32_t kvt_decode_attention_partial(const kvt_layer_cache* cache, const void* q, int32_t H_q,
                                                 const int32_t* seq_len_host, const int32_t* seq_len_dev, float scale,
                                                 float* partial, void* ws, uint64_t ws_bytes, void* stream) {

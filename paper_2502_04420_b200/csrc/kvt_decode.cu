@@ -184,15 +184,15 @@ size_t decode_workspace(const Geometry& g, int H_q, int plan_len) {
     if (get_instance(g.kb, g.vb, kernel_kind(g), GM, &in, &sms) != KVT_OK) { in.occ = 4; sms = 148; }
     if (kernel_kind(g) >= 2) {
         const int n = plan_ctas(g, plan_len, in.occ, sms);
-        return n > 1 ? sk_parts_bytes(n) + counters_bytes(g) : 0;
+        return n > 1 ? counters_bytes(g) + sk_parts_bytes(n) : 0;
     }
     int ns = plan_splits(g, plan_len, in.occ, sms);
-    return ns > 1 ? parts_bytes(ns, g.B, H_q) + counters_bytes(g) : 0;
+    return ns > 1 ? counters_bytes(g) + parts_bytes(ns, g.B, H_q) : 0;
 }
 
 int32_t launch_decode(const Geometry& g, const CachePtrs& c, const uint16_t* q, int H_q, const int32_t* seq_len,
                       int plan_len, float scale, void* out, int out_mode, void* workspace, size_t ws_bytes,
-                      void* stream, float* const* push, int n_push) {
+                      void* stream, float* const* push, int n_push, bool early) {
     using namespace dec;
     const int gq = H_q / g.H;
     const int GM = gq <= 4 ? 4 : 8;
@@ -207,16 +207,19 @@ int32_t launch_decode(const Geometry& g, const CachePtrs& c, const uint16_t* q, 
     a.out = out;
     a.final_mode = out_mode;
     a.push.n = n_push;
+    a.early = early ? 1 : 0;
     for (int i = 0; i < kMaxPush; ++i) a.push.p[i] = i < n_push ? push[i] : nullptr;
     if (kind >= 2) {
         // tensor-core kernel: stream-K over all (b, kv head) units, fused merge of units cut across CTAs
         const int n = plan_ctas(g, plan_len, in.occ, sms);
-        const size_t need = n > 1 ? sk_parts_bytes(n) + counters_bytes(g) : 0;
+        const size_t need = n > 1 ? counters_bytes(g) + sk_parts_bytes(n) : 0;
         if (need > ws_bytes || (need && !workspace))
             return fail(KVT_ERR_WORKSPACE, "decode: workspace %zu < %zu bytes (use kvt_decode_workspace_bytes)", ws_bytes, need);
         a.out_mode = out_mode;
-        a.parts = (float*)workspace;
-        a.counters = n > 1 ? (int*)((char*)workspace + sk_parts_bytes(n)) : nullptr;
+        // the merge counters sit at offset 0 (their place depends only on B * H, not on this layer's CTA count,
+        // so calls with different instances can share one workspace); the partial slots follow them
+        a.counters = n > 1 ? (int*)workspace : nullptr;
+        a.parts = n > 1 ? (float*)((char*)workspace + counters_bytes(g)) : nullptr;
         a.n_split = 1;
         a.n_cta = n;
         a.trace = nullptr;
@@ -249,11 +252,12 @@ int32_t launch_decode(const Geometry& g, const CachePtrs& c, const uint16_t* q, 
         return KVT_OK;
     }
     int ns = plan_splits(g, plan_len, in.occ, sms);
-    size_t need = ns > 1 ? parts_bytes(ns, g.B, H_q) + counters_bytes(g) : 0;
+    size_t need = ns > 1 ? counters_bytes(g) + parts_bytes(ns, g.B, H_q) : 0;
     if (need > ws_bytes || (need && !workspace))
         return fail(KVT_ERR_WORKSPACE, "decode: workspace %zu < %zu bytes (use kvt_decode_workspace_bytes)", ws_bytes, need);
     a.out_mode = ns > 1 ? 3 : out_mode;
-    a.parts = (float*)workspace;
+    // after the (untouched) counter region, so a tensor-core layer sharing this workspace keeps its zeroed counters
+    a.parts = ns > 1 ? (float*)((char*)workspace + counters_bytes(g)) : nullptr;
     a.n_split = ns;
     a.counters = nullptr;      // the generic kernel merges its splits with the separate combine launch
     a.n_cta = 0;
@@ -264,8 +268,7 @@ int32_t launch_decode(const Geometry& g, const CachePtrs& c, const uint16_t* q, 
     if (e != cudaSuccess) return fail(KVT_ERR_CUDA, "decode launch: %s", cudaGetErrorString(e));
     if (ns > 1) {
         int rows = g.B * H_q;
-        combine_kernel<<<(rows + 3) / 4, 128, 0, (cudaStream_t)stream>>>((const float*)workspace, ns, rows, out, out_mode,
-                                                                          a.push);
+        combine_kernel<<<(rows + 3) / 4, 128, 0, (cudaStream_t)stream>>>(a.parts, ns, rows, out, out_mode, a.push);
         e = cudaGetLastError();
         if (e != cudaSuccess) return fail(KVT_ERR_CUDA, "combine launch: %s", cudaGetErrorString(e));
     }

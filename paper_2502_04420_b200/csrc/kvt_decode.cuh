@@ -75,6 +75,8 @@ struct DecodeArgs {
     unsigned long long* trace;   // KVT_TRACE builds only: per-CTA (SM, start, end); else null
     int n_cta;         // tensor-core kernel: stream-K CTAs (parts [n_cta][2][8][D + 2], counters [B][H_kv])
     PushList push;     // out_mode 2 with push.n > 0: the partial rows go to every push.p[i] (a6 fused exchange)
+    int early;         // 1: the prologue (length scan, q setup) may run before griddepcontrol.wait — only when the
+                       // library itself launched the preceding kernel (kvt_append_decode_attention); 0: wait first
 };
 
 // Stream-K cost of one (b, kv head) unit of the tensor-core kernel (kvt_decode_mma.cuh)

@@ -374,9 +374,10 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
                 qg[gg][j] = acc;
             }
     }
-    // Everything above reads only q and the lengths, which the producer of q wrote before the append kernel
-    // that precedes this launch started; the launch is a programmatic dependent of that append (PDL), so
-    // the prologue above overlaps it.  The cache (records, residuals) is read only after the wait.
+    // Everything above reads only q and the lengths.  With a.early (kvt_append_decode_attention) they were written
+    // before the append kernel that precedes this launch started, and the launch is a programmatic dependent of
+    // that append (PDL), so the prologue above overlaps it; otherwise the kernel already waited at entry.  The
+    // cache (records, residuals) is read only after the wait.
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     Slice tl = sl;
     if (PAGED) {
@@ -1084,6 +1085,10 @@ __global__ void __launch_bounds__(kThreads, GM == 4 ? 4 : 3) decode_mma_kernel(D
     __shared__ long long s_first[2];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int B = a.g.B, H = a.g.H;
+    // Programmatic dependent launch: unless the library launched the preceding kernel itself (the append of
+    // kvt_append_decode_attention, which leaves q and the lengths untouched), nothing may be read before the
+    // preceding grid's writes are visible.
+    if (!a.early) asm volatile("griddepcontrol.wait;\n" ::: "memory");
     // (1) exclusive scan of the per-batch costs H * cost(S_b): thread = a chunk of consecutive b
     const int chunk = (B + kThreads - 1) / kThreads;
     const int b0 = min(tid * chunk, B), b1 = min(b0 + chunk, B);

@@ -77,7 +77,8 @@ int32_t launch_append(const Geometry& g, const CachePtrs& c, const uint16_t* k_n
 // out_mode: 0 = final bf16, 1 = final fp32, 2 = partial (m, l, o) fp32 [B][H_q][d+2]
 int32_t launch_decode(const Geometry& g, const CachePtrs& c, const uint16_t* q, int H_q,
                       const int32_t* seq_len, int plan_len, float scale, void* out, int out_mode,
-                      void* workspace, size_t ws_bytes, void* stream, float* const* push = nullptr, int n_push = 0);
+                      void* workspace, size_t ws_bytes, void* stream, float* const* push = nullptr, int n_push = 0,
+                      bool early = false);
 size_t decode_workspace(const Geometry& g, int H_q, int plan_len);
 int32_t launch_combine(const float* parts, int n_parts, int B, int H_q, int d, void* out, int out_dtype,
                        void* stream);

@@ -72,6 +72,8 @@ def _load():
                                       i32, P]),
         "kvt_decode_workspace_bytes": (i32, [ctypes.POINTER(_Cache), i32, P, ctypes.POINTER(u64)]),
         "kvt_decode_attention": (i32, [ctypes.POINTER(_Cache), P, i32, P, P, ctypes.c_float, P, i32, P, u64, P]),
+        "kvt_append_decode_attention": (i32, [ctypes.POINTER(_Cache), P, P, ctypes.POINTER(ctypes.c_int64), P, P, i32,
+                                              P, i32, P, ctypes.c_float, P, i32, P, u64, P]),
         "kvt_decode_attention_partial": (i32, [ctypes.POINTER(_Cache), P, i32, P, P, ctypes.c_float, P, P, u64,
                                                P]),
         "kvt_decode_attention_partial_push": (i32, [ctypes.POINTER(_Cache), P, i32, P, P, ctypes.c_float,
@@ -102,7 +104,7 @@ EXPORTED = ("kvt_abi_version", "kvt_status_string", "kvt_last_error", "kvt_confi
             "kvt_decode_workspace_bytes", "kvt_decode_attention", "kvt_decode_attention_partial",
             "kvt_combine_partials", "kvt_sensitivity_workspace_bytes", "kvt_layer_sensitivity",
             "kvt_pareto_prune", "kvt_dbscan", "kvt_prune_and_cluster", "kvt_search_space_log10", "kvt_page_bytes",
-            "kvt_decode_attention_partial_push")
+            "kvt_decode_attention_partial_push", "kvt_append_decode_attention")
 
 
 def lib():
@@ -130,6 +132,36 @@ def _dev(t: torch.Tensor, name: str, dtype=None):
     if dtype is not None and t.dtype != dtype:
         raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
     return t
+
+
+def _check_lengths(cache: "LayerCache", t: torch.Tensor, name: str):
+    """int32 CUDA tensor with at least `batch` entries (the kernels read batch of them)."""
+    _dev(t, name, torch.int32)
+    if not t.is_contiguous() or t.numel() < cache.batch:
+        raise ValueError(f"{name} must be a contiguous int32 tensor with >= {cache.batch} entries")
+
+
+def _check_q(cache: "LayerCache", q: torch.Tensor) -> int:
+    """q must be [batch][g * kv_heads][head_dim] for this cache; returns H_q."""
+    if q.dim() != 3 or q.shape[0] != cache.batch or q.shape[2] != cache.head_dim or q.shape[1] % cache.kv_heads:
+        raise ValueError(f"q must be [batch={cache.batch}][g*{cache.kv_heads}][{cache.head_dim}], got {tuple(q.shape)}")
+    return q.shape[1]
+
+
+def _check_new(cache: "LayerCache", k_new: torch.Tensor, v_new: torch.Tensor):
+    _dev(k_new, "k_new", torch.bfloat16)
+    _dev(v_new, "v_new", torch.bfloat16)
+    if k_new.dim() != 4 or k_new.shape[0] != cache.batch or k_new.shape[1] != cache.kv_heads \
+            or k_new.shape[3] != cache.head_dim:
+        raise ValueError(f"k_new must be [batch={cache.batch}][kv_heads={cache.kv_heads}][T][{cache.head_dim}], "
+                         f"got {tuple(k_new.shape)}")
+    if k_new.shape != v_new.shape or k_new.stride() != v_new.stride() or k_new.stride(-1) != 1:
+        raise ValueError("k_new and v_new need the same shape/strides with a contiguous last dim")
+
+
+def _check_out(t: torch.Tensor, shape, name: str):
+    if not t.is_cuda or not t.is_contiguous() or t.numel() < math.prod(shape):
+        raise ValueError(f"{name} must be a contiguous CUDA tensor of {list(shape)} elements")
 
 
 def _host_i32(t) -> Optional[ctypes.Array]:
@@ -261,12 +293,9 @@ def quantize_append(cache: LayerCache, k_new: torch.Tensor, v_new: torch.Tensor,
                     n_new: torch.Tensor, len_before_host=None, n_new_host=None, n_new_max: Optional[int] = None,
                     stream=None):
     """k_new/v_new: bf16 [B][H][T][d] (d contiguous); len_before/n_new: int32 [B] on the device."""
-    _dev(k_new, "k_new", torch.bfloat16)
-    _dev(v_new, "v_new", torch.bfloat16)
-    _dev(len_before, "len_before", torch.int32)
-    _dev(n_new, "n_new", torch.int32)
-    if k_new.shape != v_new.shape or k_new.stride() != v_new.stride() or k_new.stride(-1) != 1:
-        raise ValueError("k_new and v_new need the same shape/strides with a contiguous last dim")
+    _check_new(cache, k_new, v_new)
+    _check_lengths(cache, len_before, "len_before")
+    _check_lengths(cache, n_new, "n_new")
     strides = (ctypes.c_int64 * 3)(k_new.stride(0), k_new.stride(1), k_new.stride(2))
     if n_new_max is None:
         n_new_max = k_new.shape[2]
@@ -290,16 +319,18 @@ def decode_attention(cache: LayerCache, q: torch.Tensor, seq_len: torch.Tensor, 
                      out_dtype=torch.float32, workspace: Optional[torch.Tensor] = None, stream=None):
     """q: bf16 [B][H_q][d]; seq_len: int32 [B] (device).  Returns out [B][H_q][d] (fp32 or bf16)."""
     _dev(q, "q", torch.bfloat16)
-    _dev(seq_len, "seq_len", torch.int32)
+    _check_lengths(cache, seq_len, "seq_len")
+    H_q = _check_q(cache, q)
     q = q.contiguous()
-    B, H_q, d = q.shape
+    B, _, d = q.shape
     if scale is None:
         scale = 1.0 / math.sqrt(d)                          # A9
     if out is None:
         out = torch.empty(B, H_q, d, dtype=out_dtype, device=q.device)
     od = 1 if out.dtype == torch.float32 else 0
-    if out.dtype not in (torch.float32, torch.bfloat16) or not out.is_contiguous():
+    if out.dtype not in (torch.float32, torch.bfloat16):
         raise ValueError("out must be a contiguous fp32 or bf16 tensor")
+    _check_out(out, (B, H_q, d), "out")
     if workspace is None:
         nb = decode_workspace_bytes(cache, H_q, seq_len_host)
         workspace = torch.zeros(max(nb, 16), dtype=torch.uint8, device=q.device)   # counters start at zero
@@ -309,17 +340,53 @@ def decode_attention(cache: LayerCache, q: torch.Tensor, seq_len: torch.Tensor, 
     return out
 
 
+def append_decode_attention(cache: LayerCache, k_new: torch.Tensor, v_new: torch.Tensor, len_before: torch.Tensor,
+                            n_new: torch.Tensor, q: torch.Tensor, seq_len: torch.Tensor, n_new_max: int = 1,
+                            scale: Optional[float] = None, out: Optional[torch.Tensor] = None,
+                            out_dtype=torch.float32, workspace: Optional[torch.Tensor] = None, stream=None):
+    """One layer's serving step (kvt_append_decode_attention): append k_new/v_new [B][H][T][d] (n_new[b] <= T
+    tokens of each sequence, T <= n_new_max) and attend with q over seq_len (= len_before + n_new, the caller's)
+    tokens.  No host lengths: capturable once in a CUDA graph."""
+    _check_new(cache, k_new, v_new)
+    for t, n in ((len_before, "len_before"), (n_new, "n_new"), (seq_len, "seq_len")):
+        _check_lengths(cache, t, n)
+    _dev(q, "q", torch.bfloat16)
+    H_q = _check_q(cache, q)
+    q = q.contiguous()
+    B, _, d = q.shape
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)
+    if out is None:
+        out = torch.empty(B, H_q, d, dtype=out_dtype, device=q.device)
+    if out.dtype not in (torch.float32, torch.bfloat16):
+        raise ValueError("out must be a contiguous fp32 or bf16 tensor")
+    _check_out(out, (B, H_q, d), "out")
+    if workspace is None:
+        nb = decode_workspace_bytes(cache, H_q, None)
+        workspace = torch.zeros(max(nb, 16), dtype=torch.uint8, device=q.device)
+    strides = (ctypes.c_int64 * 3)(k_new.stride(0), k_new.stride(1), k_new.stride(2))
+    _check(_lib.kvt_append_decode_attention(ctypes.byref(cache._c), _ptr(k_new), _ptr(v_new), strides, _ptr(len_before),
+                                            _ptr(n_new), int(n_new_max), _ptr(q), H_q, _ptr(seq_len), float(scale),
+                                            _ptr(out), 1 if out.dtype == torch.float32 else 0, _ptr(workspace),
+                                            workspace.numel(), ctypes.c_void_p(_stream(stream))))
+    return out
+
+
 def decode_attention_partial(cache: LayerCache, q: torch.Tensor, seq_len: torch.Tensor, seq_len_host=None,
                              scale: Optional[float] = None, partial: Optional[torch.Tensor] = None,
                              workspace: Optional[torch.Tensor] = None, stream=None):
     """Partial (m, l, o) fp32 [B][H_q][d + 2] over this shard's tokens (a6)."""
     _dev(q, "q", torch.bfloat16)
+    _check_lengths(cache, seq_len, "seq_len")
+    H_q = _check_q(cache, q)
     q = q.contiguous()
-    B, H_q, d = q.shape
+    B, _, d = q.shape
     if scale is None:
         scale = 1.0 / math.sqrt(d)
     if partial is None:
         partial = torch.empty(B, H_q, d + 2, dtype=torch.float32, device=q.device)
+    _dev(partial, "partial", torch.float32)
+    _check_out(partial, (B, H_q, d + 2), "partial")
     if workspace is None:
         nb = decode_workspace_bytes(cache, H_q, seq_len_host)
         workspace = torch.zeros(max(nb, 16), dtype=torch.uint8, device=q.device)
@@ -336,8 +403,10 @@ def decode_attention_partial_push(cache: LayerCache, q: torch.Tensor, seq_len: t
     every destination of `dsts` (1..8 fp32 tensors, or raw device addresses, e.g. this shard's slot of each
     peer's symmetric-memory gathered buffer)."""
     _dev(q, "q", torch.bfloat16)
+    _check_lengths(cache, seq_len, "seq_len")
+    H_q = _check_q(cache, q)
     q = q.contiguous()
-    B, H_q, d = q.shape
+    B, _, d = q.shape
     if scale is None:
         scale = 1.0 / math.sqrt(d)
     ptrs = []

@@ -41,9 +41,12 @@ def shard_spec(spec, rank: int, world: int):
     return spec if rank == world - 1 else replace(spec, residual=0)
 
 
-def _all_gather(part: torch.Tensor, group=None) -> torch.Tensor:
+def _all_gather(part: torch.Tensor, group=None, gathered: Optional[torch.Tensor] = None) -> torch.Tensor:
+    if not dist.is_initialized():                          # one shard, no process group: nothing to exchange
+        return part.unsqueeze(0)
     world = dist.get_world_size(group)
-    gathered = torch.empty((world,) + tuple(part.shape), dtype=part.dtype, device=part.device)
+    if gathered is None:
+        gathered = torch.empty((world,) + tuple(part.shape), dtype=part.dtype, device=part.device)
     try:
         dist.all_gather_into_tensor(gathered, part.contiguous(), group=group)
     except (RuntimeError, NotImplementedError):
@@ -53,22 +56,30 @@ def _all_gather(part: torch.Tensor, group=None) -> torch.Tensor:
 
 def sharded_decode(cache, q: torch.Tensor, seq_len: torch.Tensor, seq_len_host=None, group=None,
                    out_dtype=torch.bfloat16, partial_fn: Optional[Callable] = None,
-                   combine_fn: Optional[Callable] = None, scale: Optional[float] = None):
+                   combine_fn: Optional[Callable] = None, scale: Optional[float] = None,
+                   out: Optional[torch.Tensor] = None, part: Optional[torch.Tensor] = None,
+                   gathered: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None,
+                   stream=None, after_partial: Optional[Callable] = None):
     """One layer of sequence-sharded decode attention on this rank; returns the full output on every rank.
 
     partial_fn / combine_fn default to the library's kernels; tests inject CPU stand-ins to exercise
-    the orchestration (shard layout, gather order) on a gloo process group."""
+    the orchestration (shard layout, gather order) on a gloo process group.  `part`, `gathered`, `out`
+    and `workspace` are optional preallocated buffers (the benchmark's step reuses them every layer);
+    `after_partial` is called right after the partial launch (the benchmark records a CUDA event there)."""
     if partial_fn is None:
         from . import kvt
 
-        part = kvt.decode_attention_partial(cache, q, seq_len, seq_len_host=seq_len_host, scale=scale)
+        part = kvt.decode_attention_partial(cache, q, seq_len, seq_len_host=seq_len_host, scale=scale,
+                                            partial=part, workspace=workspace, stream=stream)
     else:
         part = partial_fn(cache, q, seq_len)
-    gathered = _all_gather(part, group)
+    if after_partial is not None:
+        after_partial()
+    gathered = _all_gather(part, group, gathered)
     if combine_fn is None:
         from . import kvt
 
-        return kvt.combine_partials(gathered, out_dtype=out_dtype)
+        return kvt.combine_partials(gathered, out=out, out_dtype=out_dtype, stream=stream)
     return combine_fn(gathered)
 
 
@@ -90,12 +101,14 @@ class SymmExchange:
         self.k = 0
 
     def decode(self, cache, q, seq_len, seq_len_host=None, scale=None, out=None, out_dtype=torch.bfloat16,
-               workspace=None, stream=None):
+               workspace=None, stream=None, after_partial: Optional[Callable] = None):
         from . import kvt
 
         k = self.k
         kvt.decode_attention_partial_push(cache, q, seq_len, self.slots[k], seq_len_host=seq_len_host, scale=scale,
                                           workspace=workspace, stream=stream)
+        if after_partial is not None:
+            after_partial()
         self.handle.barrier(channel=0)
         self.k ^= 1
         return kvt.combine_partials(self.buf[k], out=out, out_dtype=out_dtype, stream=stream)

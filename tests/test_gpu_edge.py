@@ -1,0 +1,218 @@
+"""GPU parity on the value edge cases of Eq. 2 and of the decode kernel's fp16 normalisation
+(VERDICT r1 item 1c, W3): the CUDA path through the C ABI against the oracle on
+
+* groups cycling through constant, all-zero (+0 / -0), range 1e-3 .. 1e-6, N(0, 1) and exact-tie grids, so
+  constant / zero groups (stored s = 0, A2) sit next to tiny-range groups in every tile, for K and V, in the
+  KIVI and per-token layouts (kvt_synth.edge_structured);
+* whole caches of tiny values (1e-36, and 2e-38 near the bf16 / fp32 min-normal 1.18e-38) and wide values (1e4);
+* attention-sink heads (q aligned with token 0's key) and q with a 2^±20 dynamic range.
+
+K1 must be bit-exact on every defined byte; K2's fp32 output within 2e-3 normalised (A17).
+Also: one workspace shared by layers of different precision pairs / CTA counts, the fused
+kvt_append_decode_attention against the two separate calls, and the binding's shape validation.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import kvt_synth
+from tests.gpu_helpers import TOL, compare_slice, rel_row_err
+
+pytestmark = pytest.mark.gpu
+D = 128
+
+
+@pytest.fixture(scope="module")
+def kvt():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2502_04420_b200 as k
+
+    return k
+
+
+SPECS = [
+    ("kivi_k4v2", lambda k: k.LayerSpec.kivi(4, 2)),
+    ("kivi_k8v4", lambda k: k.LayerSpec.kivi(8, 4)),
+    ("kivi_k2v2", lambda k: k.LayerSpec.kivi(2, 2)),
+    ("kivi_k2v8", lambda k: k.LayerSpec.kivi(2, 8)),
+    ("pt_k8v4", lambda k: k.LayerSpec.per_token(8, 4)),
+    ("pt_k4v2", lambda k: k.LayerSpec.per_token(4, 2)),
+    ("pt_k2v2_r32", lambda k: k.LayerSpec.per_token(2, 2, residual=32)),
+    ("pt_k8v2_g64", lambda k: k.LayerSpec.per_token(8, 2, group=64)),        # generic CUDA-core kernel
+    ("kivi_k4v4_g128", lambda k: k.LayerSpec.kivi(4, 4, group=128, residual=128)),
+]
+LENS = [1000, 257, 64, 33, 1]
+
+
+def _kv(kind, spec, B, H, S, seed):
+    if kind == "structured":
+        along_k = "channel" if spec.mode == 1 else "token"
+        K = kvt_synth.edge_structured((B, H, S, D), seed, along_k)
+        V = kvt_synth.edge_structured((B, H, S, D), seed + 1, "token")
+    elif kind == "tiny":
+        K = (1e-36 * torch.randn(B, H, S, D, generator=kvt_synth.generator(seed))).to(torch.bfloat16)
+        V = (1e-36 * torch.randn(B, H, S, D, generator=kvt_synth.generator(seed + 1))).to(torch.bfloat16)
+    elif kind == "minnormal":
+        K = (2e-38 * torch.randn(B, H, S, D, generator=kvt_synth.generator(seed))).to(torch.bfloat16)
+        V = (2e-38 * torch.randn(B, H, S, D, generator=kvt_synth.generator(seed + 1))).to(torch.bfloat16)
+    elif kind == "wide":
+        K = kvt_synth.special_rows("wide", (B, H, S, D), seed)
+        V = kvt_synth.special_rows("wide", (B, H, S, D), seed + 1)
+    else:
+        raise ValueError(kind)
+    return K, V
+
+
+def _prefill(kvt, spec, K, V, lens):
+    B, H = K.shape[:2]
+    cap = ((max(lens) + 127) // 128) * 128
+    cache = kvt.LayerCache(spec, B, H, D, cap)
+    kvt.quantize_append(cache, K.cuda(), V.cuda(), torch.zeros(B, dtype=torch.int32, device="cuda"),
+                        torch.tensor(lens, dtype=torch.int32, device="cuda"), len_before_host=[0] * B, n_new_host=lens)
+    return cache
+
+
+def _check(kvt, oracle, spec, K, V, q, lens, g, check_bytes=True):
+    B, H = K.shape[:2]
+    cache = _prefill(kvt, spec, K, V, lens)
+    sl = torch.tensor(lens, dtype=torch.int32, device="cuda")
+    out = kvt.decode_attention(cache, q.cuda(), sl, seq_len_host=lens, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    Kb, Vb, qb = kvt_synth.bf16_bits(K), kvt_synth.bf16_bits(V), kvt_synth.bf16_bits(q)
+    o = out.cpu().numpy()
+    assert np.isfinite(o).all()
+    worst = 0.0
+    for b, S in enumerate(lens):
+        for h in range(H):
+            if check_bytes:
+                compare_slice(oracle, cache, spec, b, h, Kb[b, h, :S], Vb[b, h, :S], S)
+            rows = slice(h * g, (h + 1) * g)
+            ref = oracle.decode_reference(spec.mode, spec.key_bits, spec.value_bits, spec.group, spec.residual, D,
+                                          Kb[b, h, :S], Vb[b, h, :S], qb[b, rows], 1 / math.sqrt(D))
+            err = rel_row_err(o[b, rows], ref)
+            worst = max(worst, float(err.max()))
+            assert err.max() <= TOL, f"b={b} h={h} S={S}: normalised error {err.max():.3e}"
+    return worst
+
+
+@pytest.mark.parametrize("kind", ["structured", "tiny", "minnormal", "wide"])
+@pytest.mark.parametrize("name,mk", SPECS, ids=[s[0] for s in SPECS])
+def test_edge_values(kvt, oracle, name, mk, kind):
+    spec = mk(kvt)
+    B, H, g = len(LENS), 2, 4
+    K, V = _kv(kind, spec, B, H, max(LENS), seed=900)
+    q = kvt_synth.queries((B, H * g, D), seed=903)
+    _check(kvt, oracle, spec, K, V, q, LENS, g)
+
+
+@pytest.mark.parametrize("name,mk", SPECS, ids=[s[0] for s in SPECS])
+def test_q_dynamic_range(kvt, oracle, name, mk):
+    """q spanning 2^-30 .. 2^14 (per-head 2^±20, per-channel 2^±10) on structured K / V."""
+    spec = mk(kvt)
+    B, H, g = len(LENS), 2, 7
+    K, V = _kv("structured", spec, B, H, max(LENS), seed=910)
+    q = kvt_synth.edge_queries((B, H * g, D), seed=913)
+    _check(kvt, oracle, spec, K, V, q, LENS, g, check_bytes=False)
+
+
+@pytest.mark.parametrize("name,mk", SPECS, ids=[s[0] for s in SPECS])
+def test_sink_heads(kvt, oracle, name, mk):
+    """Attention sinks: heads 0 and 2 of every group have q = 0.25 * k_0, so token 0 takes most
+    of the softmax mass; the other heads are ordinary."""
+    spec = mk(kvt)
+    B, H, g = len(LENS), 2, 4
+    K = kvt_synth.keys((B, H, max(LENS), D), seed=920)
+    V = kvt_synth.values((B, H, max(LENS), D), seed=921)
+    q = kvt_synth.queries((B, H * g, D), seed=922).float()
+    for h in range(H):
+        for j in (0, 2):
+            q[:, h * g + j] = 0.25 * K[:, h, 0].float()
+    _check(kvt, oracle, spec, K, V, q.to(torch.bfloat16), LENS, g, check_bytes=False)
+
+
+def test_workspace_shared_across_instances(kvt, oracle):
+    """layers with different CTA counts (K4V2: 4 CTAs/SM, K8V4: 3) share one workspace at
+    B * H_kv above the slot count, so both run stream-K with cut units; every layer's output must equal a run on
+    its own fresh workspace (same partition: bitwise) and the oracle."""
+    B, H, g, S = 80, 8, 4, 700          # 640 units > 592 slots
+    K = kvt_synth.keys((B, H, S, D), seed=930).cuda()
+    V = kvt_synth.values((B, H, S, D), seed=931).cuda()
+    q = kvt_synth.queries((B, H * g, D), seed=932).cuda()
+    sl = torch.full((B,), S, dtype=torch.int32, device="cuda")
+    specs = [kvt.LayerSpec.kivi(4, 2), kvt.LayerSpec.kivi(8, 4), kvt.LayerSpec.kivi(4, 2), kvt.LayerSpec.kivi(8, 4)]
+    caches = [_prefill(kvt, s, K, V, [S] * B) for s in specs]
+    nb = max(kvt.decode_workspace_bytes(c, H * g, None) for c in caches)
+    shared = torch.zeros(nb, dtype=torch.uint8, device="cuda")
+    outs = [kvt.decode_attention(c, q, sl, out_dtype=torch.float32, workspace=shared) for c in caches]
+    fresh = [kvt.decode_attention(c, q, sl, out_dtype=torch.float32,
+                                  workspace=torch.zeros(nb, dtype=torch.uint8, device="cuda")) for c in caches]
+    torch.cuda.synchronize()
+    for a, b in zip(outs, fresh):
+        assert torch.equal(a, b)
+    Kb, Vb, qb = kvt_synth.bf16_bits(K), kvt_synth.bf16_bits(V), kvt_synth.bf16_bits(q)
+    rng = np.random.default_rng(5)
+    for i, s in enumerate(specs[:2]):
+        for b, h in [(0, 0), (B - 1, H - 1)] + [(int(rng.integers(B)), int(rng.integers(H))) for _ in range(4)]:
+            ref = oracle.decode_reference(1, s.key_bits, s.value_bits, 32, 32, D, Kb[b, h], Vb[b, h],
+                                          qb[b, h * g:(h + 1) * g], 1 / math.sqrt(D))
+            assert rel_row_err(outs[i][b, h * g:(h + 1) * g].cpu().numpy(), ref).max() <= TOL
+    assert shared[:4 * B * H].view(torch.int32).abs().sum().item() == 0      # counters left at zero
+
+
+@pytest.mark.parametrize("mk,g", [(lambda k: k.LayerSpec.kivi(4, 2), 4), (lambda k: k.LayerSpec.per_token(8, 4), 7),
+                                  (lambda k: k.LayerSpec.per_token(4, 4, group=64), 4)])
+def test_append_decode_fused_equals_separate(kvt, mk, g):
+    """kvt_append_decode_attention == kvt_quantize_append + kvt_decode_attention, bitwise (same kernels, same
+    plan), over several steps at B * H filling the GPU (so the tensor-core launch uses PDL)."""
+    spec = mk(kvt)
+    B, H, S0, steps = 96, 8, 300, 3
+    K = kvt_synth.keys((B, H, S0 + steps, D), seed=940).cuda()
+    V = kvt_synth.values((B, H, S0 + steps, D), seed=941).cuda()
+    q = kvt_synth.queries((B, H * g, D), seed=942).cuda()
+    cap = 384
+    ca = _prefill(kvt, spec, K[:, :, :S0].contiguous(), V[:, :, :S0].contiguous(), [S0] * B)
+    cb = _prefill(kvt, spec, K[:, :, :S0].contiguous(), V[:, :, :S0].contiguous(), [S0] * B)
+    assert ca.capacity == cap
+    ws = [torch.zeros(max(kvt.decode_workspace_bytes(c, H * g, None), 16), dtype=torch.uint8, device="cuda")
+          for c in (ca, cb)]
+    ones = torch.ones(B, dtype=torch.int32, device="cuda")
+    for i in range(steps):
+        lb = torch.full((B,), S0 + i, dtype=torch.int32, device="cuda")
+        la = lb + 1
+        kn, vn = K[:, :, S0 + i:S0 + i + 1], V[:, :, S0 + i:S0 + i + 1]
+        kvt.quantize_append(ca, kn, vn, lb, ones, n_new_max=1)
+        a = kvt.decode_attention(ca, q, la, out_dtype=torch.float32, workspace=ws[0])
+        b = kvt.append_decode_attention(cb, kn, vn, lb, ones, q, la, out_dtype=torch.float32, workspace=ws[1])
+        torch.cuda.synchronize()
+        assert torch.equal(a, b)
+    for name in ca.buffers:
+        if ca.buffers[name] is not None:
+            assert torch.equal(ca.buffers[name], cb.buffers[name])
+
+
+def test_binding_rejects_bad_shapes(kvt):
+    """the binding validates shapes before any launch."""
+    spec = kvt.LayerSpec.kivi(4, 2)
+    cache = kvt.LayerCache(spec, 4, 2, D, 64)
+    sl = torch.full((4,), 10, dtype=torch.int32, device="cuda")
+    with pytest.raises(ValueError):
+        kvt.decode_attention(cache, torch.zeros(3, 8, D, dtype=torch.bfloat16, device="cuda"), sl)   # batch 3 != 4
+    with pytest.raises(ValueError):
+        kvt.decode_attention(cache, torch.zeros(4, 7, D, dtype=torch.bfloat16, device="cuda"), sl)   # 7 % 2 != 0
+    with pytest.raises(ValueError):
+        kvt.decode_attention(cache, torch.zeros(4, 8, D, dtype=torch.bfloat16, device="cuda"), sl.long())
+    with pytest.raises(ValueError):
+        kvt.decode_attention(cache, torch.zeros(4, 8, D, dtype=torch.bfloat16, device="cuda"), sl[:3])
+    with pytest.raises(ValueError):
+        kvt.decode_attention(cache, torch.zeros(4, 8, D, dtype=torch.bfloat16, device="cuda"), sl,
+                             out=torch.zeros(4, 4, D, device="cuda"))
+    with pytest.raises(ValueError):
+        kvt.decode_attention_partial(cache, torch.zeros(4, 8, D, dtype=torch.bfloat16, device="cuda"), sl,
+                                     partial=torch.zeros(4, 8, D, device="cuda"))                 # needs d + 2
+    with pytest.raises(ValueError):
+        kvt.quantize_append(cache, torch.zeros(4, 3, 1, D, dtype=torch.bfloat16, device="cuda"),
+                            torch.zeros(4, 3, 1, D, dtype=torch.bfloat16, device="cuda"),
+                            sl, torch.ones(4, dtype=torch.int32, device="cuda"))               # kv_heads 3 != 2

@@ -24,11 +24,15 @@ def kvt():
     return k
 
 
-@pytest.mark.parametrize("kb,vb,H,g,B", [(4, 2, 8, 4, 64), (8, 4, 8, 4, 64), (2, 2, 8, 4, 64), (8, 8, 4, 7, 32),
-                                         (4, 4, 4, 7, 32)])
-def test_fullsize_sampled(kvt, oracle, kb, vb, H, g, B):
+# (mode, kb, vb, H, g, B): Llama-3.1-8B shape (H = 8, g = 4) with the KIVI 3.25 map's pairs; Qwen2.5-7B shape
+# (H = 4, g = 7) with the 4.00 map's pairs in the KIVI layout (A19) and in its own per-token mode, at B = 64
+@pytest.mark.parametrize("mode,kb,vb,H,g,B", [(1, 4, 2, 8, 4, 64), (1, 8, 4, 8, 4, 64), (1, 2, 2, 8, 4, 64),
+                                              (1, 4, 4, 8, 4, 64), (1, 8, 8, 4, 7, 64), (1, 4, 4, 4, 7, 64),
+                                              (1, 8, 2, 4, 7, 64), (0, 8, 8, 4, 7, 64), (0, 8, 2, 4, 7, 64),
+                                              (0, 4, 4, 4, 7, 64), (0, 4, 2, 4, 7, 64)])
+def test_fullsize_sampled(kvt, oracle, mode, kb, vb, H, g, B):
     S0, n_dec = 8191, 3                      # prefill 8191 tokens, then 3 decode steps (crosses a K flush)
-    spec = kvt.LayerSpec.kivi(kb, vb)
+    spec = kvt.LayerSpec.kivi(kb, vb) if mode == 1 else kvt.LayerSpec.per_token(kb, vb)
     cap = 8192 + 64
     dev = torch.device("cuda")
     gen = torch.Generator(device=dev).manual_seed(1234 + kb * 10 + vb)
@@ -55,7 +59,7 @@ def test_fullsize_sampled(kvt, oracle, kb, vb, H, g, B):
         Kb = kvt_synth.bf16_bits(K[b, h, :S])
         Vb = kvt_synth.bf16_bits(V[b, h, :S])
         compare_slice(oracle, cache, spec, b, h, Kb, Vb, S)
-        ref = oracle.decode_reference(spec.mode, kb, vb, 32, 32, D, Kb, Vb,
+        ref = oracle.decode_reference(spec.mode, kb, vb, 32, spec.residual, D, Kb, Vb,
                                       kvt_synth.bf16_bits(q[b, h * g:(h + 1) * g]), 1 / math.sqrt(D))
         err = rel_row_err(out[b, h * g:(h + 1) * g].cpu().numpy(), ref)
         assert err.max() <= TOL, f"(b={b}, h={h}): normalised error {err.max():.2e}"
