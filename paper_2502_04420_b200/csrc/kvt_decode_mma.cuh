@@ -83,9 +83,12 @@ __device__ __forceinline__ float fexp2(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
 }
-__device__ __forceinline__ int frexp_e(float x) {           // x = f 2^e, f in [0.5, 1); clamped
+// x = f 2^e, f in [0.5, 1), e clamped to [-119, 90] (subnormal x: -119).  Every power of two the kernel derives
+// from it (2^(7-e), 2^(e-7), 2^(17+e), 2^(24-6-(7-e)) ...) is then a normal fp32, so scales anywhere in bf16's
+// range down to its subnormals normalise without underflow (values above 2^90 are outside the supported range).
+__device__ __forceinline__ int frexp_e(float x) {
     const int e = x > 0.0f ? (int)((__float_as_uint(x) >> 23) & 0xFF) - 126 : 0;
-    return e < -90 ? -90 : (e > 90 ? 90 : e);
+    return e < -119 ? -119 : (e > 90 ? 90 : e);
 }
 __device__ __forceinline__ float pow2(int e) { return __uint_as_float((uint32_t)(127 + e) << 23); }
 
@@ -845,16 +848,12 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
             smb = __reduce_max_sync(kFull, smb);
             const int kt = 7 - frexp_e(bf2f(smb));
             if (kt < kp) {
-                if (it > 0) { kfac = pow2(kt - kp); resc = true; }
+                if (it > 0) { kfac = pow2(kt - kp < -126 ? -126 : kt - kp); resc = true; }
                 kp = kt;
             }
+            // 2^kp is folded into the value scale (s_v 2^kp <= 2^7 for every bf16 scale), not into p (<= 2^8), so
+            // no product overflows even at kp = 126; powers of two multiply exactly, so the weights are the same
             const float ksc = pow2(kp);
-            float2 pk[2][2];           // (p(T), p(T+8)) * 2^kp for heads j: pk[mt][j]
-#pragma unroll
-            for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-                for (int j = 0; j < 2; ++j)
-                    pk[mt][j] = dec::fmul2(make_float2(p[mt][0][j], p[mt][1][j]), make_float2(ksc, ksc));
             // weight-tile word of (group gsh + gr, m-tile mt): one per-lane base plus a compile-time offset (gsh is
             // even, so 4 ((gsh + gr) >> 1) = 4 (gsh >> 1) for GM == 4; gsh = 0 for GM == 8)
             uint32_t* const wst = w_s + (gsh * 2 * 8 + gid) * 8 + 4 * (gsh >> 1) + hA;
@@ -868,9 +867,10 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
 #pragma unroll
                 for (int mt = 0; mt < 2; ++mt) {
                     const uint32_t w0 = mw[mt][0][gr], w1 = mw[mt][1][gr];
-                    const float2 sv = make_float2(bf2f(w0 & 0xffffu), bf2f(w1 & 0xffffu));
+                    const float2 sv = dec::fmul2(make_float2(bf2f(w0 & 0xffffu), bf2f(w1 & 0xffffu)), make_float2(ksc, ksc));
                     uint2 wv;
-                    const float2 wa = dec::fmul2(pk[mt][0], sv), wb = dec::fmul2(pk[mt][1], sv);
+                    const float2 wa = dec::fmul2(make_float2(p[mt][0][0], p[mt][1][0]), sv);
+                    const float2 wb = dec::fmul2(make_float2(p[mt][0][1], p[mt][1][1]), sv);
                     wv.x = h2u(__floats2half2_rn(wa.x, wa.y));
                     wv.y = h2u(__floats2half2_rn(wb.x, wb.y));
                     *reinterpret_cast<uint2*>(wst + (gr * 2 + mt) * 64 + (GM == 4 ? 0 : 4 * (gr >> 1))) = wv;

@@ -2,7 +2,7 @@
 (VERDICT r1 item 1c, W3): the CUDA path through the C ABI against the oracle on
 
 * groups cycling through constant, all-zero (+0 / -0), range 1e-3 .. 1e-6, N(0, 1) and exact-tie grids, so
-  constant / zero groups (stored s = 0, A2) sit next to tiny-range groups in every tile, for K and V, in the
+  constant / zero groups (A2: stored s = 1, codes 0) sit next to tiny-range groups in every tile, for K and V, in the
   KIVI and per-token layouts (kvt_synth.edge_structured);
 * whole caches of tiny values (1e-36, and 2e-38 near the bf16 / fp32 min-normal 1.18e-38) and wide values (1e4);
 * attention-sink heads (q aligned with token 0's key) and q with a 2^±20 dynamic range.
@@ -70,6 +70,9 @@ def _prefill(kvt, spec, K, V, lens):
     B, H = K.shape[:2]
     cap = ((max(lens) + 127) // 128) * 128
     cache = kvt.LayerCache(spec, B, H, D, cap)
+    for buf in cache.buffers.values():          # bytes the layout leaves undefined compare equal between caches
+        if buf is not None:
+            buf.zero_()
     kvt.quantize_append(cache, K.cuda(), V.cuda(), torch.zeros(B, dtype=torch.int32, device="cuda"),
                         torch.tensor(lens, dtype=torch.int32, device="cuda"), len_before_host=[0] * B, n_new_host=lens)
     return cache
