@@ -224,7 +224,7 @@ def test_sequence_shards_combine(kvt, oracle, n_shards):
     assert (out - ref_gpu).abs().max().item() <= 5e-4 * ref_gpu.abs().max().item()
 
 
-@pytest.mark.parametrize("mode,R", [(0, 0), (1, 32), (2, 0)])
+@pytest.mark.parametrize("mode,R", [(0, 0), (0, 32), (0, 64), (1, 32), (1, 64), (2, 0)])
 def test_sensitivity_parity(kvt, oracle, mode, R):
     H_kv, g, S, T_q = 2, 4, 256, 24
     K = kvt_synth.keys((H_kv, S, D), seed=51)

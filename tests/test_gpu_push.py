@@ -92,3 +92,52 @@ def test_symmetric_memory_exchange_one_rank(kvt):
             assert rel_row_err(out.cpu().numpy(), ref.cpu().numpy()).max() <= 1e-6
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n_shards", [2, 4])
+def test_virtual_shards_push_against_oracle(kvt, oracle, n_shards):
+    """a6 + NEXT #2 on one GPU with N virtual ranks: shard r = tokens [r S/N, (r+1) S/N) of every
+    sequence (seqshard.shard_bounds / shard_spec: residual on the last shard only) pushes its (m, l, o) rows into slot r
+    of two "peer" buffers [N][B][H_q][D+2] (what kvt_decode_attention_partial_push writes over NVLink in a real run);
+    each peer's kvt_combine_partials must equal the unsharded fp64 oracle (Eq. 1 over the whole cache), and the two
+    peers must agree bit for bit."""
+    import math
+
+    import numpy as np
+
+    from paper_2502_04420_b200.seqshard import shard_bounds, shard_spec
+    from tests.gpu_helpers import TOL
+
+    B, H, g, S = 2, 2, 4, 1500
+    base = kvt.LayerSpec.kivi(4, 2)
+    K = kvt_synth.keys((B, H, S, D), seed=811)
+    V = kvt_synth.values((B, H, S, D), seed=812)
+    q = kvt_synth.queries((B, H * g, D), seed=813)
+    peers = [torch.full((n_shards, B, H * g, D + 2), float("nan"), device="cuda") for _ in range(2)]
+    for r in range(n_shards):
+        lo, hi = shard_bounds(S, n_shards, r)
+        spec = shard_spec(base, r, n_shards)
+        n = hi - lo
+        cache = _cache_from(kvt, spec, K[:, :, lo:hi].contiguous(), V[:, :, lo:hi].contiguous(), n)
+        sl = torch.full((B,), n, dtype=torch.int32, device="cuda")
+        kvt.decode_attention_partial_push(cache, q.cuda(), sl, [p[r] for p in peers], seq_len_host=[n] * B)
+    outs = [kvt.combine_partials(p, out_dtype=torch.float32) for p in peers]
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
+    Kb, Vb, qb = kvt_synth.bf16_bits(K), kvt_synth.bf16_bits(V), kvt_synth.bf16_bits(q)
+    o = outs[0].cpu().numpy()
+    for b in range(B):
+        for h in range(H):
+            ref = oracle.decode_reference(1, 4, 2, 32, 32, D, Kb[b, h], Vb[b, h], qb[b, h * g:(h + 1) * g],
+                                          1 / math.sqrt(D))
+            assert rel_row_err(o[b, h * g:(h + 1) * g], ref).max() <= TOL
+
+
+def _cache_from(kvt, spec, K, V, n):
+    B, H = K.shape[:2]
+    cap = ((n + 63) // 64) * 64
+    cache = kvt.LayerCache(spec, B, H, D, cap)
+    kvt.quantize_append(cache, K.cuda(), V.cuda(), torch.zeros(B, dtype=torch.int32, device="cuda"),
+                        torch.full((B,), n, dtype=torch.int32, device="cuda"), len_before_host=[0] * B,
+                        n_new_host=[n] * B)
+    return cache

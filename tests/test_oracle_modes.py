@@ -93,3 +93,22 @@ def test_pc_direction_channel_outliers(oracle):
         assert pt[i, 0] > 1.5 * pc[i, 0]            # e_k: per-token clearly worse (paper: 2.5x at INT8)
         assert pt[i, 2] > pc[i, 2]                  # e_a follows the key error
         assert 0.5 < pt[i, 1] / pc[i, 1] < 2.0      # e_v: "quite close" across dimensions
+
+
+def test_pt_residual_rows_are_exact(oracle):
+    """Per-token-asym with a full-precision residual window (A6, T-Mode P:619-647 at R > 0): the last R tokens are
+    kept as they are, the others quantised row by row exactly as with R = 0.  So with R >= S every error is 0, and
+    with 0 < R < S the key / value errors are the R = 0 errors of the first S - R rows diluted by S / (S - R)
+    (e_k, e_v average |x - x_hat| / |x| over all elements; the residual rows contribute exact zeros)."""
+    H_kv, g, S, T_q, d, R = 2, 4, 256, 24, 128, 64
+    Q, K, V = _qkv(H_kv, g, S, T_q, d, seed=71)
+    pairs = [(2, 2), (4, 2), (8, 4)]
+    scale = 1 / math.sqrt(d)
+    full = oracle.sensitivity(PT, 32, S, Q, K, V, S - T_q, pairs, scale)
+    assert np.all(full == 0.0)
+    with_r = oracle.sensitivity(PT, 32, R, Q, K, V, S - T_q, pairs, scale)
+    head = oracle.sensitivity(PT, 32, 0, Q, np.ascontiguousarray(K[:, :S - R]), np.ascontiguousarray(V[:, :S - R]),
+                              S - R - T_q, pairs, scale)
+    np.testing.assert_allclose(with_r[:, 0], head[:, 0] * (S - R) / S, rtol=1e-12)     # e_k
+    np.testing.assert_allclose(with_r[:, 1], head[:, 1] * (S - R) / S, rtol=1e-12)     # e_v
+    assert np.all(with_r[:, 3] > 0) and np.all(with_r[:, 3] < head[:, 3] * 4)          # e_o: still quantised
