@@ -323,18 +323,27 @@ class OracleSampler:
         return dt, n_units / (L * H)
 
 
-def cpu_baseline_record(sampler, S):
-    """cpu_baseline at 1 core and at nproc cores: bounded samples of the workload."""
+def cpu_baseline_record(sampler, S, single_s=5.0, multi_s=12.0):
+    """cpu_baseline at 1 core and at nproc cores: bounded samples of the workload, sized by time
+    (~5 s single-core, ~12 s on all cores, so the default run stays within minutes)."""
     hi = host_info()
     n = hi["nproc"] or 1
-    dt1, tok1 = sampler.run(16, 1)
-    dtn, tokn = sampler.run(2 * n, n)
+    dt1 = tok1 = 0.0
+    n1 = 0
+    while dt1 < single_s:
+        dt, tok = sampler.run(4, 1)
+        dt1 += dt; tok1 += tok; n1 += 4
+    dtn = tokn = 0.0
+    nn = 0
+    while dtn < multi_s:
+        dt, tok = sampler.run(2 * n, n)
+        dtn += dt; tokn += tok; nn += 2 * n
     return {"value": tokn / dtn, "unit": "tokens/s", "cores": n, "kind": "oracle",
-            "sample": f"{2 * n} (layer, kv head) units of 1 sequence at S={S} on {n} threads "
+            "sample": f"{nn} (layer, kv head) units of 1 sequence at S={S} on {n} threads "
                       f"(= {tokn:.3f} decode tokens, {dtn:.1f} s); oracle = O2 static build + fp64 read-back "
                       f"+ fp64 Eq.1, plain C, one unit per thread",
             "single_core": {"value": tok1 / dt1, "unit": "tokens/s", "cores": 1,
-                            "sample": f"16 units at S={S} ({dt1:.1f} s)"},
+                            "sample": f"{n1} units at S={S} ({dt1:.1f} s)"},
             **hi}
 
 
@@ -423,8 +432,6 @@ def run_kvt(args):
     # ---- build the caches: prefill S0 tokens per sequence through the append kernel ----
     gen = torch.Generator(device=dev)
     caches = []
-    len0 = torch.zeros(B, dtype=torch.int32, device=dev)
-    nS0 = torch.full((B,), S0, dtype=torch.int32, device=dev)
     for l, spec in enumerate(specs):
         if args.paged:        # vLLM-style: one block table per layer, pages assigned in a random order
             pg = torch.Generator().manual_seed(500 + l)
@@ -433,13 +440,20 @@ def run_kvt(args):
         else:
             cache = kvt.LayerCache(spec, B, H, D, cap, device=dev)
         gen.manual_seed(1000 * rank + l)
-        Kp = torch.randn(B, H, S0, D, device=dev, generator=gen)
-        Kp[..., ::8] *= 11.0                                  # kvt_synth recipe: key channel outliers
-        Kp = Kp.to(torch.bfloat16)
-        Vp = torch.randn(B, H, S0, D, device=dev, generator=gen).to(torch.bfloat16)
-        kvt.quantize_append(cache, Kp, Vp, len0, nS0, len_before_host=[0] * B, n_new_host=[S0] * B)
-        del Kp, Vp
-        torch.cuda.empty_cache()                              # large batches: keep the prefill temporaries from fragmenting HBM
+        # prefill in token chunks (the append is history independent, A7) so the bf16/fp32 temporaries stay at
+        # ~1.5 GB whatever the batch: the config-4 sweep fills ~90% of HBM with the cache itself
+        pf = max(32, min(S0, int(1.5e9 / (B * H * D * 6))) // 32 * 32)
+        for t0 in range(0, S0, pf):
+            n = min(pf, S0 - t0)
+            Kp = torch.randn(B, H, n, D, device=dev, generator=gen)
+            Kp[..., ::8] *= 11.0                              # kvt_synth recipe: key channel outliers
+            Kp = Kp.to(torch.bfloat16)
+            Vp = torch.randn(B, H, n, D, device=dev, generator=gen).to(torch.bfloat16)
+            kvt.quantize_append(cache, Kp, Vp, torch.full((B,), t0, dtype=torch.int32, device=dev),
+                                torch.full((B,), n, dtype=torch.int32, device=dev), len_before_host=[t0] * B,
+                                n_new_host=[n] * B)
+            del Kp, Vp
+        torch.cuda.empty_cache()
         caches.append(cache)
     torch.cuda.synchronize()
     # ---- per-step inputs (resident): one contiguous device buffer of every layer's q, k_new, v_new and one of
