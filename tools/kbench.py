@@ -19,9 +19,11 @@ ap.add_argument("--g", type=int, default=4)
 ap.add_argument("--S", type=int, default=8192)
 ap.add_argument("--reps", type=int, default=30)
 ap.add_argument("--pt", action="store_true", help="per-token-asym keys (default KIVI)")
+ap.add_argument("--group", type=int, default=32, help="G (64/128: the generic CUDA-core kernel)")
 a = ap.parse_args()
 dev = torch.device("cuda")
-spec = kvt.LayerSpec.per_token(a.kb, a.vb) if a.pt else kvt.LayerSpec.kivi(a.kb, a.vb)
+spec = (kvt.LayerSpec.per_token(a.kb, a.vb, group=a.group) if a.pt
+        else kvt.LayerSpec.kivi(a.kb, a.vb, group=a.group, residual=max(32, a.group)))
 cap = ((a.S + 63) // 64) * 64
 cache = kvt.LayerCache(spec, a.B, a.H, 128, cap)
 gen = torch.Generator(device=dev).manual_seed(1)
@@ -50,5 +52,5 @@ for i in range(a.reps + 3):
 ts.sort()
 med = ts[len(ts) // 2]
 nbytes = sum(cache.sizes[n] for n in ("k_codes", "k_meta", "v_codes", "v_meta")) * a.S / cap
-print(f"{os.environ.get('KVT_LIB', 'libkvt.so'):22s} {'PT ' if a.pt else ''}K{a.kb}V{a.vb} g={a.g} B={a.B} S={a.S}: {med * 1000:8.1f} us  "
+print(f"{os.environ.get('KVT_LIB', 'libkvt.so'):22s} {'PT ' if a.pt else ''}K{a.kb}V{a.vb} G={a.group} g={a.g} B={a.B} S={a.S}: {med * 1000:8.1f} us  "
       f"{nbytes / med / 1e6:7.1f} GB/s (min {ts[0] * 1000:.1f})")
