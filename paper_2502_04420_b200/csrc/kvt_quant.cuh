@@ -45,13 +45,16 @@ __device__ __forceinline__ GroupQ group_params(float mn, float mx, int bits) {
     return q;
 }
 
+// clamp(rint(t), 0, qmax): cvt.rni to an unsigned integer rounds to nearest even and saturates negatives to 0
+__device__ __forceinline__ uint32_t rint_clamp(float t, uint32_t qmax) {
+    const uint32_t c = __float2uint_rn(t);
+    return c < qmax ? c : qmax;
+}
+
 __device__ __forceinline__ uint32_t code_of(float x, const GroupQ& q) {
-    if (q.degenerate) return 0u;
-    float t = __fmul_rn(__fsub_rn(x, q.mn), q.inv);
-    float r = rintf(t);
-    r = fmaxf(r, 0.0f);
-    r = fminf(r, q.qmax);
-    return (uint32_t)r;
+    // degenerate groups have inv = 0, so t = 0 and the code is 0 (A2) without a branch
+    const float t = __fmul_rn(__fsub_rn(x, q.mn), q.inv);
+    return rint_clamp(t, (uint32_t)q.qmax);
 }
 
 __device__ __forceinline__ void unpack4(uint2 v, float x[4]) {
@@ -139,11 +142,8 @@ __device__ __forceinline__ void quant_rows8_warp(const uint2 v[8], int nrow, int
         const float z = __shfl_sync(kFull, q.mn, (lane & 24) | r);
         uint32_t packed = 0;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            float t = rintf(__fmul_rn(__fsub_rn(x[r][i], z), inv));
-            t = fminf(fmaxf(t, 0.0f), q.qmax);
-            packed |= (uint32_t)t << (i * bits);
-        }
+        for (int i = 0; i < 4; ++i)
+            packed |= rint_clamp(__fmul_rn(__fsub_rn(x[r][i], z), inv), (uint32_t)q.qmax) << (i * bits);
         dst.store(r, lane, bits, packed);
     }
 }
