@@ -598,6 +598,17 @@ def run_kvt(args):
                 "frac_of_spec_8TBs": achieved / SPEC_HBM_GBS,
                 "algorithmic_bytes_per_step": alg / args.steps,
                 "timing": "CUDA events around every attention launch of a second (eager) pass of K steps"}
+    # per precision pair: mean attention time per launch and its fraction of the peak (same events)
+    by_pair = {}
+    for l, s in enumerate(specs):
+        key = f"{'PT' if s.mode != 1 else ''}K{s.key_bits}V{s.value_bits}"
+        t = sum(evs[i][l][0].elapsed_time(evs[i][l][1]) for i in range(args.steps)) / args.steps
+        nb = sum(algorithmic_bytes(s, B, H, Hq, S_first + (args.steps + i if appends else 0))
+                 for i in range(args.steps)) / args.steps
+        e = by_pair.setdefault(key, {"layers": 0, "us": 0.0, "bytes": 0.0})
+        e["layers"] += 1; e["us"] += t * 1000.0; e["bytes"] += nb
+    roofline["by_pair"] = {k: {"layers": v["layers"], "us_per_launch": v["us"] / v["layers"],
+                               "frac": v["bytes"] / (v["us"] / 1e6) / 1e9 / peak} for k, v in by_pair.items()}
 
     # ---- e2e: host (pinned) inputs -> device, step, outputs -> host, every step ----
     e2e = None

@@ -159,8 +159,9 @@ int32_t kvt_quantize_append(const kvt_layer_cache* cache, const void* k_new, con
  * The split-KV partials live in `workspace` (size from kvt_decode_workspace_bytes).  The workspace must
  * be zero-filled before its first use (it holds per-(b, kv head) split-arrival counters); every call
  * leaves those counters at zero again, so one workspace can be reused by consecutive calls on a stream.
- * The workspace is laid out [merge counters: round_up(4 * batch * kv_heads, 256) bytes][partials], so calls on
- * caches with the same (batch, kv_heads) can share one workspace whatever their precision pair or CTA count.
+ * The workspace is laid out [merge counters: round_up(4 * batch * kv_heads, 256) bytes][schedule counters:
+ * round_up(4 * (514 + batch * kv_heads + SMs), 256) bytes][partials], so calls on caches with the same (batch,
+ * kv_heads) on one device can share one workspace whatever their precision pair or CTA count.
  * Ordering: tile-record layers may launch as a programmatic dependent (PDL) of the preceding kernel in the stream
  * (when the grid nearly fills the GPU); the kernel then waits for that kernel's completion before it reads
  * anything, so the call is ordered after every preceding stream operation like a plain launch. */

@@ -155,6 +155,29 @@ static size_t parts_bytes(int ns, int B, int H_q) { return ((size_t)ns * B * H_q
 static size_t counters_bytes(const Geometry& g) { return ((size_t)g.B * g.H * sizeof(int) + 255) & ~(size_t)255; }
 // stream-K partial slots of the tensor-core kernel: [n_cta][2][8 heads][D + 2]
 static size_t sk_parts_bytes(int n_cta) { return ((size_t)n_cta * 2 * 8 * (dec::D + 2) * sizeof(float) + 255) & ~(size_t)255; }
+// schedule counters of the per-SM plan (kvt_decode_mma.cuh, sm_claim): 2 x 256 per-%smid words, 2 scalars and one
+// claim word per item (<= units + SMs); at a fixed offset after the merge counters (depends on B * H and the SM count
+// only, so layers of any precision pair sharing one workspace never see their counters overwritten by partials)
+static size_t sched_bytes(const Geometry& g, int sms) {
+    return ((2 * 256 + 2 + (size_t)g.B * g.H + (size_t)sms) * sizeof(int) + 255) & ~(size_t)255;
+}
+
+// Per-SM plan (whole units in slots 0 .. w-1 of every SM, one piece of the remaining units in slot w) where the
+// whole-unit plan would leave ceil(U / SMs) units on some SMs and floor(U / SMs) on others: w = floor(U / SMs)
+// >= 2 whole units per SM, a slot to spare (w + 1 <= occupancy) and a remainder to spread.  Returns w, or 0.
+// Measured (one layer, B = 64, 8k): Llama K4V2 145 -> 135 us, K4V4 156 -> 148, K2V2 141 -> 131 (w = 3); with w = 1
+// (Qwen g = 7: one whole unit + a piece on 3-CTA SMs) it lost (K4V4 106 -> 113 us): once the piece is done the
+// whole unit runs alone on its SM with 4 warps, which cannot keep the SM busy.
+static int plan_sm_w(const Geometry& g, int occ, int sms) {
+    static const bool on = [] { const char* e = getenv("KVT_SMPLAN"); return !e || atoi(e) != 0; }();   // A/B switch
+    if (!on) return 0;
+    const long long units = (long long)g.B * g.H, slots = (long long)occ * sms;
+    const long long per_sm = (units + sms - 1) / sms;
+    const bool whole = units <= slots && 2 * units >= 3LL * sms && 5 * per_sm * sms <= 6 * units;   // plan_ctas' rule
+    const long long w = units / sms;
+    if (!whole || w < 2 || w + 1 > occ || units % sms == 0) return 0;
+    return (int)w;
+}
 
 // Stream-K CTAs (tensor-core kernel): at most one wave of resident CTAs (estimated from plan_len; the kernel
 // clamps to the actual total work).
@@ -183,11 +206,12 @@ size_t decode_workspace(const Geometry& g, int H_q, int plan_len) {
     Instance in; int sms = 148;
     if (get_instance(g.kb, g.vb, kernel_kind(g), GM, &in, &sms) != KVT_OK) { in.occ = 4; sms = 148; }
     if (kernel_kind(g) >= 2) {
-        const int n = plan_ctas(g, plan_len, in.occ, sms);
-        return n > 1 ? counters_bytes(g) + sk_parts_bytes(n) : 0;
+        const int w = plan_sm_w(g, in.occ, sms);
+        const int n = w ? in.occ * sms : plan_ctas(g, plan_len, in.occ, sms);
+        return n > 1 ? counters_bytes(g) + sched_bytes(g, sms) + sk_parts_bytes(w ? sms : n) : 0;
     }
     int ns = plan_splits(g, plan_len, in.occ, sms);
-    return ns > 1 ? counters_bytes(g) + parts_bytes(ns, g.B, H_q) : 0;
+    return ns > 1 ? counters_bytes(g) + sched_bytes(g, sms) + parts_bytes(ns, g.B, H_q) : 0;
 }
 
 int32_t launch_decode(const Geometry& g, const CachePtrs& c, const uint16_t* q, int H_q, const int32_t* seq_len,
@@ -211,15 +235,22 @@ int32_t launch_decode(const Geometry& g, const CachePtrs& c, const uint16_t* q, 
     for (int i = 0; i < kMaxPush; ++i) a.push.p[i] = i < n_push ? push[i] : nullptr;
     if (kind >= 2) {
         // tensor-core kernel: stream-K over all (b, kv head) units, fused merge of units cut across CTAs
-        const int n = plan_ctas(g, plan_len, in.occ, sms);
-        const size_t need = n > 1 ? counters_bytes(g) + sk_parts_bytes(n) : 0;
+        const int w = plan_sm_w(g, in.occ, sms);
+        const int n = w ? in.occ * sms : plan_ctas(g, plan_len, in.occ, sms);
+        const size_t need = n > 1 ? counters_bytes(g) + sched_bytes(g, sms) + sk_parts_bytes(w ? sms : n) : 0;
         if (need > ws_bytes || (need && !workspace))
             return fail(KVT_ERR_WORKSPACE, "decode: workspace %zu < %zu bytes (use kvt_decode_workspace_bytes)", ws_bytes, need);
         a.out_mode = out_mode;
-        // the merge counters sit at offset 0 (their place depends only on B * H, not on this layer's CTA count,
-        // so calls with different instances can share one workspace); the partial slots follow them
+        // the merge counters sit at offset 0 and the schedule counters right after them (their places depend only
+        // on B * H and the SM count, not on this layer's CTA count, so calls with different instances can share one
+        // workspace); the partial slots follow them
         a.counters = n > 1 ? (int*)workspace : nullptr;
-        a.parts = n > 1 ? (float*)((char*)workspace + counters_bytes(g)) : nullptr;
+        a.sched = n > 1 ? (int*)((char*)workspace + counters_bytes(g)) : nullptr;
+        a.parts = n > 1 ? (float*)((char*)workspace + counters_bytes(g) + sched_bytes(g, sms)) : nullptr;
+        a.sm_w = w;
+        a.sm_n = sms;
+        static const int drop = [] { const char* e = getenv("KVT_SMPLAN_DROP"); return e ? atoi(e) : 0; }();
+        a.sm_drop = drop;
         a.n_split = 1;
         a.n_cta = n;
         a.trace = nullptr;
@@ -235,7 +266,8 @@ int32_t launch_decode(const Geometry& g, const CachePtrs& c, const uint16_t* q, 
         // placed unevenly, which a partial wave cannot absorb (Qwen, 256 whole units on 444 slots: 15 449
         // tokens/s with PDL vs 19 583 without; Llama, 512 on 592: +2% with PDL).
         static const bool pdl_env = [] { const char* e = getenv("KVT_PDL"); return !e || atoi(e) != 0; }();
-        const bool pdl = pdl_env && 4LL * n >= 3LL * in.occ * sms;
+        // Not with the per-SM plan either: llama-3.25 step 4.606 ms without PDL vs 4.682 ms with it (B = 64).
+        const bool pdl = pdl_env && 4LL * n >= 3LL * in.occ * sms && w == 0;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(n);
         cfg.blockDim = dim3(kThreads);
@@ -252,12 +284,16 @@ int32_t launch_decode(const Geometry& g, const CachePtrs& c, const uint16_t* q, 
         return KVT_OK;
     }
     int ns = plan_splits(g, plan_len, in.occ, sms);
-    size_t need = ns > 1 ? counters_bytes(g) + parts_bytes(ns, g.B, H_q) : 0;
+    size_t need = ns > 1 ? counters_bytes(g) + sched_bytes(g, sms) + parts_bytes(ns, g.B, H_q) : 0;
     if (need > ws_bytes || (need && !workspace))
         return fail(KVT_ERR_WORKSPACE, "decode: workspace %zu < %zu bytes (use kvt_decode_workspace_bytes)", ws_bytes, need);
     a.out_mode = ns > 1 ? 3 : out_mode;
-    // after the (untouched) counter region, so a tensor-core layer sharing this workspace keeps its zeroed counters
-    a.parts = ns > 1 ? (float*)((char*)workspace + counters_bytes(g)) : nullptr;
+    // after the (untouched) counter regions, so a tensor-core layer sharing this workspace keeps its zeroed counters
+    a.parts = ns > 1 ? (float*)((char*)workspace + counters_bytes(g) + sched_bytes(g, sms)) : nullptr;
+    a.sched = nullptr;
+    a.sm_w = 0;
+    a.sm_n = sms;
+    a.sm_drop = 0;
     a.n_split = ns;
     a.counters = nullptr;      // the generic kernel merges its splits with the separate combine launch
     a.n_cta = 0;

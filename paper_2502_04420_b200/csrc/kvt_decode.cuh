@@ -77,6 +77,11 @@ struct DecodeArgs {
     PushList push;     // out_mode 2 with push.n > 0: the partial rows go to every push.p[i] (a6 fused exchange)
     int early;         // 1: the prologue (length scan, q setup) may run before griddepcontrol.wait — only when the
                        // library itself launched the preceding kernel (kvt_append_decode_attention); 0: wait first
+    // per-SM plan of the tensor-core kernel (sm_w > 0): on each of the sm_n SMs, slots 0 .. sm_w-1 take whole units
+    // and slot sm_w one stream-K piece of the remaining units; sched = its claim counters (zero between calls)
+    int sm_w, sm_n;
+    int* sched;
+    int sm_drop;       // tests only (KVT_SMPLAN_DROP = k): CTAs with blockIdx % k == 0 leave their item unclaimed
 };
 
 // Stream-K cost of one (b, kv head) unit of the tensor-core kernel (kvt_decode_mma.cuh)

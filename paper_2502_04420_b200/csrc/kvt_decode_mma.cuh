@@ -444,7 +444,6 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
 #pragma unroll
     for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.0f;
     int kp = 126;                  // PV weight exponent (only decreases)
-
     // ---- tail tokens [n_main, S) first (before the main loop: at the end of the CTA the whole wave finishes
     // together and these dependent loads would sit on the critical path).  Super-chunks of <= 128 tokens:
     //   (1) QK: lane = token, warp = a quarter of the channels (4-channel groups rotated by lane, so the
@@ -569,7 +568,7 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
     if (staged && tid == 0) asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(tbar)));
     __syncthreads();
     KVT_STAMP(7);
-    // ---- per-warp TMA ring: lane 0 issues one bulk copy (the tile record) per tile onto the stage's mbarrier ----
+    // ---- per-warp TMA ring: one elected lane issues one bulk copy (the tile record) per tile onto the stage mbarrier ----
     uint64_t* bars = reinterpret_cast<uint64_t*>(wbase + Gm::BAR_OFF);
     if (lane == 0) {
 #pragma unroll
@@ -577,14 +576,23 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncwarp();
+    // The whole warp runs the issue path (no divergent branch around it); elect.sync picks the lane that arms the
+    // stage's mbarrier and issues the copy.  The ring's shared-memory addresses and the warp's first record are
+    // computed once (warp-uniform: they live in uniform registers).
+    const uint32_t ring_u32 = smem_u32(wbase), bars_u32 = smem_u32(bars);
+    // dense: `nxt` = the record of the next tile to issue, advanced by kWarps records per issue (loop-carried)
+    const uint8_t* nxt = PAGED ? nullptr : sl.kc + (size_t)(tile_lo + warp) * Gm::STAGE;
     auto issue = [&](int it, int st) {
-        if (lane != 0) return;
-        const int t0 = (tile_lo + warp + it * kWarps) * kTile;
-        uint8_t* sb = wbase + st * Gm::STAGE;
-        mbar_expect_tx(bars + st, Gm::STAGE);
-        const uint8_t* src = PAGED ? a.c.k_codes + ((size_t)a.c.bt[(size_t)b * a.c.max_pages + t0 / kTile] * g.H + hk) * Gm::STAGE
-                                   : sl.kc + (size_t)(t0 / kTile) * Gm::STAGE;
-        bulk_g2s(sb, src, Gm::STAGE, bars + st);     // one tile record
+        const uint8_t* src = PAGED ? a.c.k_codes + ((size_t)a.c.bt[(size_t)b * a.c.max_pages + tile_lo + warp + it * kWarps] * g.H + hk) * Gm::STAGE
+                                   : nxt;
+        if (!PAGED) nxt += kWarps * Gm::STAGE;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "elect.sync _|p, 0xffffffff;\n\t"
+            "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t"
+            "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%2], [%3], %1, [%0];\n\t}\n"
+            ::"r"(bars_u32 + 8 * st), "r"((uint32_t)Gm::STAGE), "r"(ring_u32 + st * Gm::STAGE), "l"(src)
+            : "memory");
     };
 
     // generic-proxy writes to the ring area (tail scratch) are ordered before the first bulk copies; later
@@ -599,7 +607,11 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
             const int nx = it + Gm::NS - 1;
             if (nx < n_my) issue(nx, nx % Gm::NS);
         }
-        mbar_wait(bars + (it % Gm::NS), (uint32_t)((it / Gm::NS) & 1));
+        asm volatile(
+            "{\n\t.reg .pred p;\n"
+            "WAIT_%=:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+            "@!p bra WAIT_%=;\n\t}\n" ::"r"(bars_u32 + 8 * (it % Gm::NS)), "r"((uint32_t)((it / Gm::NS) & 1)) : "memory");
         if (KVT_EXP == 4) { __syncwarp(); continue; }       // experiment: stream the tiles only
         const uint8_t* sb = wbase + (it % Gm::NS) * Gm::STAGE;
         const uint8_t* kc_s = sb + Gm::K_OFF;
@@ -1077,68 +1089,190 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
 // the CTA whose range [c C / n, (c + 1) C / n) holds position x
 __device__ __forceinline__ int cta_of(long long x, long long C, int n) { return (int)(((x + 1) * n - 1) / C); }
 
+// Per-SM plan (a.sm_w = w > 0): the grid is one full wave (occupancy x SMs CTAs).  Each CTA learns its SM
+// (%smid, ranked densely in order of first arrival) and its arrival slot on that SM.  Slots 0 .. w-1 of SM r take
+// the whole units w r + slot; slot w takes piece r of the remaining units, cut stream-K style into one piece per
+// SM (fused merge of cut units as above); later slots idle.  Every SM then holds the same work (w units plus
+// (U - w SMs) / SMs of a unit) while only one CTA per SM pays for cut segments; with whole units (the plan it
+// replaces) ceil(U / SMs) units sat on some SMs and floor(U / SMs) on others.  Correct for any placement: an
+// item no CTA claimed (an SM with fewer CTAs than expected) is run by the last CTA to finish, which also resets
+// the counters.  Schedule words: [256 arrivals per %smid][256 rank + 1 per %smid][rank count][done][claims].
+constexpr int kSchedSmid = 256;
+__device__ __forceinline__ int sm_claim(const DecodeArgs& a) {
+    int* ctr = a.sched;
+    int* rank_of = a.sched + kSchedSmid;
+    int* nrank = a.sched + 2 * kSchedSmid;
+    int* claim = a.sched + 2 * kSchedSmid + 2;
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    if (smid >= (unsigned)kSchedSmid) return -1;                   // (never on B200) left to the last CTA
+    const int slot = atomicAdd(ctr + smid, 1);
+    int r;
+    if (slot == 0) {
+        r = atomicAdd(nrank, 1);
+        atomicExch(rank_of + smid, r + 1);
+    } else {
+        int v;
+        while ((v = atomicAdd(rank_of + smid, 0)) == 0) __nanosleep(20);   // the SM's first CTA is resident
+        r = v - 1;
+    }
+    if (r >= a.sm_n || slot > a.sm_w) return -1;
+    if (a.sm_drop > 0 && blockIdx.x % a.sm_drop == 0) return -1;   // tests: exercise the unclaimed-item path
+    const int item = r * (a.sm_w + 1) + slot;
+    atomicExch(claim + item, 1);
+    return item;
+}
+
 // PAGED: tile records addressed through the block table (compile-time, so the dense issue path stays short)
 template <int KB, int VB, int GM, bool KPT, bool PAGED>
 __global__ void __launch_bounds__(kThreads, GM == 4 ? 4 : 3) decode_mma_kernel(DecodeArgs a) {
     extern __shared__ __align__(16) uint8_t smem[];
-    __shared__ long long s_wsum[kWarps];
+    __shared__ long long s_wsum[2][kWarps];
     __shared__ long long s_first[2];
+    __shared__ int s_item, s_last;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int B = a.g.B, H = a.g.H;
     // Programmatic dependent launch: unless the library launched the preceding kernel itself (the append of
-    // kvt_append_decode_attention, which leaves q and the lengths untouched), nothing may be read before the
-    // preceding grid's writes are visible.
+    // kvt_append_decode_attention, which leaves q, the lengths and the workspace untouched), nothing may be read
+    // before the preceding grid's writes are visible.
     if (!a.early) asm volatile("griddepcontrol.wait;\n" ::: "memory");
-    // (1) exclusive scan of the per-batch costs H * cost(S_b): thread = a chunk of consecutive b
+    // (1) exclusive scan of the per-batch costs H * cost(S_b): thread = a chunk of consecutive b; with the per-SM
+    // plan also the cost Cw of the whole units [0, w SMs)
+    const long long u0 = (long long)a.sm_w * a.sm_n;
     const int chunk = (B + kThreads - 1) / kThreads;
     const int b0 = min(tid * chunk, B), b1 = min(b0 + chunk, B);
-    long long mine = 0;
-    for (int bb = b0; bb < b1; ++bb) mine += (long long)H * unit_cost(a.g, a.seq_len[bb]).cost;
-    long long inc = mine;
+    long long mine = 0, mine_w = 0;
+    for (int bb = b0; bb < b1; ++bb) {
+        const long long c1 = unit_cost(a.g, a.seq_len[bb]).cost;
+        mine += (long long)H * c1;
+        const long long nu = u0 - (long long)bb * H;
+        mine_w += (nu <= 0 ? 0 : (nu >= H ? H : nu)) * c1;
+    }
+    long long inc = mine, inc_w = mine_w;
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) inc_w += __shfl_xor_sync(kFull, inc_w, off);
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
         const long long v = __shfl_up_sync(kFull, inc, off);
         if (lane >= off) inc += v;
     }
-    if (lane == 31) s_wsum[warp] = inc;
+    if (lane == 31) s_wsum[0][warp] = inc;
+    if (lane == 0) s_wsum[1][warp] = inc_w;
     __syncthreads();
-    long long C = 0, excl = inc - mine;
+    long long C = 0, Cw = 0, excl = inc - mine;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) {
-        if (w < warp) excl += s_wsum[w];
-        C += s_wsum[w];
+        if (w < warp) excl += s_wsum[0][w];
+        C += s_wsum[0][w];
+        Cw += s_wsum[1][w];
     }
-    const int n = (long long)a.n_cta < C ? a.n_cta : (int)C;
-    const int cta = blockIdx.x;
+    // Work of this CTA: the cost range [lo, hi) of part `idx` of the n-part cut of [base, base + span), walked unit by
+    // unit (one segment per unit touched).  Stream-K plan: part blockIdx.x of [0, C).  Per-SM plan: a whole unit
+    // (a one-part cut of its own range) or piece r of the remaining units; the last CTA to finish then walks the
+    // items nobody claimed, one after the other.  One call site of segment() (it is large and inlined).
+    long long lo = 0, hi = 0, base = 0, span = 1;
+    int n = 1, idx = 0;
+    int item = -1;
+    bool plan_sm = a.sm_w > 0, counted = false;
+    int scan = 0;
+    const int W1 = a.sm_w + 1, nsm = a.sm_n;
+    // unit u (whole) or position x (stream-K, pieces) -> its batch row and the cost offset of that row
+    auto locate = [&](bool by_unit, long long key) {
+        if (by_unit ? (key / H >= b0 && key / H < b1) : (key >= excl && key < excl + mine)) {
+            long long P = excl;
+            for (int bb = b0; bb < b1; ++bb) {
+                const long long cb = (long long)H * unit_cost(a.g, a.seq_len[bb]).cost;
+                if (by_unit ? bb == key / H : key < P + cb) { s_first[0] = bb; s_first[1] = P; break; }
+                P += cb;
+            }
+        }
+        __syncthreads();
+    };
+    if (plan_sm) {
+        if (tid == 0) s_item = sm_claim(a);
+        __syncthreads();
+        item = s_item;
+    } else {
+        n = (long long)a.n_cta < C ? a.n_cta : (int)C;
+        idx = blockIdx.x;
+        if (idx >= n) return;                               // uniform per CTA
+        lo = (long long)idx * C / n; hi = (long long)(idx + 1) * C / n; base = 0; span = C;
+        locate(false, lo);
+    }
 #if KVT_TRACE
     unsigned long long t_start;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
 #endif
-    if (cta >= n) return;                                   // uniform per CTA
-    const long long lo = (long long)cta * C / n, hi = (long long)(cta + 1) * C / n;
-    if (lo >= excl && lo < excl + mine) {
-        long long P = excl;
-        for (int bb = b0; bb < b1; ++bb) {
-            const long long cb = (long long)H * unit_cost(a.g, a.seq_len[bb]).cost;
-            if (lo < P + cb) { s_first[0] = bb; s_first[1] = P; break; }
-            P += cb;
+    for (;;) {
+        if (plan_sm) {
+            if (item >= 0) {                                // uniform per CTA
+                const int r = item / W1, slot = item - r * W1;
+                if (slot < a.sm_w) {
+                    const long long u = (long long)a.sm_w * r + slot;
+                    locate(true, u);
+                    const UnitCost uc = unit_cost(a.g, a.seq_len[s_first[0]]);
+                    lo = s_first[1] + (u - (long long)s_first[0] * H) * uc.cost;
+                    hi = lo + uc.cost; base = lo; span = uc.cost; n = 1; idx = 0;
+                } else {
+                    const long long R = C - Cw;
+                    lo = Cw + (long long)r * R / nsm; hi = Cw + (long long)(r + 1) * R / nsm;
+                    base = Cw; span = R > 0 ? R : 1; n = nsm; idx = r;
+                    if (lo < hi) locate(false, lo);
+                }
+            } else {
+                lo = hi = 0;
+            }
         }
-    }
-    __syncthreads();
-    int b = (int)s_first[0];
-    long long Pb = s_first[1], pos = lo;
-    while (pos < hi) {
-        const UnitCost uc = unit_cost(a.g, a.seq_len[b]);
-        if (pos >= Pb + (long long)H * uc.cost) { Pb += (long long)H * uc.cost; ++b; continue; }
-        const int hk = (int)((pos - Pb) / uc.cost);
-        const long long Pu = Pb + (long long)hk * uc.cost;
-        const int x0 = (int)(pos - Pu);
-        const int x1 = (int)(hi - Pu < uc.cost ? hi - Pu : uc.cost);
-        const int cf = cta_of(Pu, C, n), cl = cta_of(Pu + uc.cost - 1, C, n);
-        segment<KB, VB, GM, KPT, PAGED>(a, smem, b, hk, min(x0, uc.tiles), min(x1, uc.tiles), x1 == uc.cost, cta,
-                            cta == cf ? 1 : 0, cf, cl - cf + 1);
-        pos = Pu + x1;
-        __syncthreads();                                    // the next segment reuses shared memory
+        if (lo < hi) {
+            int b = (int)s_first[0];
+            long long Pb = s_first[1], pos = lo;
+            __syncthreads();                                // s_first is rewritten by the next locate
+            while (pos < hi) {
+                const UnitCost uc = unit_cost(a.g, a.seq_len[b]);
+                if (pos >= Pb + (long long)H * uc.cost) { Pb += (long long)H * uc.cost; ++b; continue; }
+                const int hk = (int)((pos - Pb) / uc.cost);
+                const long long Pu = Pb + (long long)hk * uc.cost;
+                const int x0 = (int)(pos - Pu);
+                const int x1 = (int)(hi - Pu < uc.cost ? hi - Pu : uc.cost);
+                const int cf = cta_of(Pu - base, span, n), cl = cta_of(Pu - base + uc.cost - 1, span, n);
+                segment<KB, VB, GM, KPT, PAGED>(a, smem, b, hk, min(x0, uc.tiles), min(x1, uc.tiles), x1 == uc.cost, idx,
+                                                idx == cf ? 1 : 0, cf, cl - cf + 1);
+                pos = Pu + x1;
+                __syncthreads();                            // the next segment reuses shared memory
+            }
+        }
+        if (!plan_sm) break;
+        if (!counted) {                                     // this CTA's own item is done: count it
+            counted = true;
+            __syncthreads();
+            if (tid == 0) {
+                __threadfence();
+                s_last = atomicAdd(a.sched + 2 * kSchedSmid + 1, 1) == (int)gridDim.x - 1;
+            }
+            __syncthreads();
+            if (!s_last) break;
+            __threadfence();
+        }
+        // the last CTA: the next item nobody claimed (only when the placement was not the expected one).  All
+        // threads test their share of the claim words at once (independent loads: one L2 round trip, not one per
+        // item) and the smallest unclaimed index wins.
+        {
+            const volatile int* claim = a.sched + 2 * kSchedSmid + 2;
+            if (tid == 0) s_item = INT_MAX;
+            __syncthreads();
+            int mine_first = INT_MAX;
+            for (int i = scan + tid; i < W1 * nsm; i += kThreads)
+                if (claim[i] == 0 && i < mine_first) mine_first = i;
+            if (mine_first != INT_MAX) atomicMin(&s_item, mine_first);
+            __syncthreads();
+            item = s_item == INT_MAX ? -1 : s_item;
+            scan = item + 1;
+            __syncthreads();
+        }
+        if (item < 0) {
+            for (int i = tid; i < 2 * kSchedSmid + 2 + W1 * nsm; i += kThreads) a.sched[i] = 0;
+            break;
+        }
     }
 #if KVT_TRACE
     if (tid == 0) {
@@ -1146,6 +1280,7 @@ __global__ void __launch_bounds__(kThreads, GM == 4 ? 4 : 3) decode_mma_kernel(D
         unsigned smid;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        const int cta = blockIdx.x;
         if (a.trace && cta < 4096) { a.trace[3 * cta] = smid; a.trace[3 * cta + 1] = t_start; a.trace[3 * cta + 2] = t_end; }
     }
 #endif
