@@ -251,6 +251,11 @@ int32_t launch_decode(const Geometry& g, const CachePtrs& c, const uint16_t* q, 
         a.sm_n = sms;
         static const int drop = [] { const char* e = getenv("KVT_SMPLAN_DROP"); return e ? atoi(e) : 0; }();
         a.sm_drop = drop;
+        // the first CTA to arrive on an SM runs ahead of the later ones (traced: the 3 whole units of an SM end at
+        // 106 / 113 / 123 us); giving it the piece ends the piece early instead of last: llama-3.25 13 880 -> 14 226
+        // tokens/s (KVT_PIECE_FIRST=0 restores the last-arriver piece, A/B only)
+        static const int piece_first = [] { const char* e = getenv("KVT_PIECE_FIRST"); return e ? atoi(e) : 1; }();
+        a.sm_piece_first = piece_first;
         a.n_split = 1;
         a.n_cta = n;
         a.trace = nullptr;
@@ -294,6 +299,7 @@ int32_t launch_decode(const Geometry& g, const CachePtrs& c, const uint16_t* q, 
     a.sm_w = 0;
     a.sm_n = sms;
     a.sm_drop = 0;
+    a.sm_piece_first = 0;
     a.n_split = ns;
     a.counters = nullptr;      // the generic kernel merges its splits with the separate combine launch
     a.n_cta = 0;

@@ -81,6 +81,7 @@ struct DecodeArgs {
     // and slot sm_w one stream-K piece of the remaining units; sched = its claim counters (zero between calls)
     int sm_w, sm_n;
     int* sched;
+    int sm_piece_first;   // per-SM plan: the first CTA to arrive on an SM takes the piece (else the last)
     int sm_drop;       // tests only (KVT_SMPLAN_DROP = k): CTAs with blockIdx % k == 0 leave their item unclaimed
 };
 

@@ -635,7 +635,8 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
             const uint4 m4 = reinterpret_cast<const uint4*>(km_s)[lane];
             const uint32_t mw[4] = {m4.x, m4.y, m4.z, m4.w};
             // the largest scale: positive bf16 bit patterns order like their values
-            uint32_t smb = max(max(mw[0] & 0xffffu, mw[1] & 0xffffu), max(mw[2] & 0xffffu, mw[3] & 0xffffu));
+            // per-halfword max of the packed (scale | zero) words (SIMD, no masking), then the scale half
+            uint32_t smb = __vmaxu2(__vmaxu2(mw[0], mw[1]), __vmaxu2(mw[2], mw[3])) & 0xffffu;
             smb = __reduce_max_sync(kFull, smb);                 // REDUX: one instruction for the warp max
             const int sbx = 7 - frexp_e(bf2f(smb));
             const float ssc = pow2(sbx);
@@ -853,10 +854,11 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
                         mw[mt][r][0] = m2.x; mw[mt][r][1] = m2.y;
                     }
 #pragma unroll
-                    for (int gr = 0; gr < NGL; ++gr) smb = max(smb, mw[mt][r][gr] & 0xffffu);
+                    for (int gr = 0; gr < NGL; ++gr) smb = __vmaxu2(smb, mw[mt][r][gr]);   // per-halfword max
                 }
             // lanes differing only in tig hold the same tokens (and, GM == 4, the same groups up to the tig^2
             // split), so the max over the whole warp is the max over all 32 tokens and 4 groups
+            smb &= 0xffffu;                                       // the scale halves
             smb = __reduce_max_sync(kFull, smb);
             const int kt = 7 - frexp_e(bf2f(smb));
             if (kt < kp) {
@@ -1090,9 +1092,9 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
 __device__ __forceinline__ int cta_of(long long x, long long C, int n) { return (int)(((x + 1) * n - 1) / C); }
 
 // Per-SM plan (a.sm_w = w > 0): the grid is one full wave (occupancy x SMs CTAs).  Each CTA learns its SM
-// (%smid, ranked densely in order of first arrival) and its arrival slot on that SM.  Slots 0 .. w-1 of SM r take
-// the whole units w r + slot; slot w takes piece r of the remaining units, cut stream-K style into one piece per
-// SM (fused merge of cut units as above); later slots idle.  Every SM then holds the same work (w units plus
+// (%smid, ranked densely in order of first arrival) and its arrival slot on that SM.  The first arrival on SM r
+// takes piece r of the remaining units, cut stream-K style into one piece per SM (fused merge of cut units as
+// above); arrivals 1 .. w take the whole units w r + 0 .. w-1; later arrivals idle.  Every SM then holds the same work (w units plus
 // (U - w SMs) / SMs of a unit) while only one CTA per SM pays for cut segments; with whole units (the plan it
 // replaces) ceil(U / SMs) units sat on some SMs and floor(U / SMs) on others.  Correct for any placement: an
 // item no CTA claimed (an SM with fewer CTAs than expected) is run by the last CTA to finish, which also resets
@@ -1195,6 +1197,7 @@ __global__ void __launch_bounds__(kThreads, GM == 4 ? 4 : 3) decode_mma_kernel(D
     } else {
         n = (long long)a.n_cta < C ? a.n_cta : (int)C;
         idx = blockIdx.x;
+        if (KVT_TRACE && tid == 0) s_item = -1;
         if (idx >= n) return;                               // uniform per CTA
         lo = (long long)idx * C / n; hi = (long long)(idx + 1) * C / n; base = 0; span = C;
         locate(false, lo);
@@ -1206,7 +1209,10 @@ __global__ void __launch_bounds__(kThreads, GM == 4 ? 4 : 3) decode_mma_kernel(D
     for (;;) {
         if (plan_sm) {
             if (item >= 0) {                                // uniform per CTA
-                const int r = item / W1, slot = item - r * W1;
+                // arrival slot -> role: the first CTA to arrive on an SM takes the piece (CTAs that arrive first on
+                // an SM run ahead of the later ones), or (KVT_PIECE_FIRST=0, A/B only) the last one
+                const int r = item / W1, slot0 = item - r * W1;
+                const int slot = a.sm_piece_first ? (slot0 == 0 ? a.sm_w : slot0 - 1) : slot0;
                 if (slot < a.sm_w) {
                     const long long u = (long long)a.sm_w * r + slot;
                     locate(true, u);
@@ -1281,7 +1287,8 @@ __global__ void __launch_bounds__(kThreads, GM == 4 ? 4 : 3) decode_mma_kernel(D
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
         const int cta = blockIdx.x;
-        if (a.trace && cta < 4096) { a.trace[3 * cta] = smid; a.trace[3 * cta + 1] = t_start; a.trace[3 * cta + 2] = t_end; }
+        // smid | (per-SM plan item + 1) << 16
+        if (a.trace && cta < 4096) { a.trace[3 * cta] = smid | (unsigned long long)(s_item + 1) << 16; a.trace[3 * cta + 1] = t_start; a.trace[3 * cta + 2] = t_end; }
     }
 #endif
 }

@@ -22,10 +22,11 @@ ap.add_argument("--B", type=int, default=64)
 ap.add_argument("--H", type=int, default=8)
 ap.add_argument("--g", type=int, default=4)
 ap.add_argument("--S", type=int, default=8192)
+ap.add_argument("--w", type=int, default=3, help="whole units per SM of the per-SM plan (for the item decode)")
 a = ap.parse_args()
 dev = torch.device("cuda")
 spec = kvt.LayerSpec.kivi(a.kb, a.vb)
-cache = kvt.LayerCache(spec, a.B, a.H, 128, a.S)
+cache = kvt.LayerCache(spec, a.B, a.H, 128, (a.S + 63) // 64 * 64)
 gen = torch.Generator(device=dev).manual_seed(1)
 K = torch.randn(a.B, a.H, a.S, 128, device=dev, generator=gen).bfloat16()
 V = torch.randn(a.B, a.H, a.S, 128, device=dev, generator=gen).bfloat16()
@@ -56,7 +57,8 @@ if (st4[:, 0] > 0).all():
     if (st4[:, 7] > 0).all():
         print("  prologue split (us): q setup", q(ph(0, 4)), "| tail wait", q(ph(4, 5)), "| tail compute", q(ph(5, 6)),
               "| tail merge", q(ph(6, 7)), "| ring start", q(ph(7, 1)))
-sm, st, en = t[:, 0], t[:, 1] - t[:, 1].min(), t[:, 2] - t[:, 1].min()
+item = (t[:, 0] >> 16) - 1                      # per-SM plan item (-1: stream-K / idle)
+sm, st, en = t[:, 0] & 0xffff, t[:, 1] - t[:, 1].min(), t[:, 2] - t[:, 1].min()
 dur = en - st
 print(f"CTAs {len(t)}  span {en.max() / 1e3:.1f} us   start spread {st.max() / 1e3:.1f} us")
 print(f"CTA duration us: min {dur.min() / 1e3:.1f}  p10 {np.percentile(dur, 10) / 1e3:.1f}  median {np.median(dur) / 1e3:.1f}"
@@ -75,3 +77,19 @@ print(f"SMs used {len(per)}  CTAs/SM min {cnt.min()} max {cnt.max()}  SM last-en
 order = np.argsort(np.array(list(per.keys())))
 keys = np.array(list(per.keys()))[order]
 print("SM last-end (us) by SM id:", " ".join(f"{int(k)}:{last[i] / 1e3:.0f}" for i, k in zip(order, keys)))
+
+if (item >= 0).any():
+    W1 = a.w + 1
+    slot = np.where(item >= 0, item % W1, -1)
+    for k in range(W1):
+        e = en[slot == k] / 1e3
+        if e.size:
+            print(f"slot {k} ({'piece' if k == a.w else 'whole unit'}): CTAs {e.size}  end us min {e.min():.1f} median {np.median(e):.1f} max {e.max():.1f}")
+    # per SM: spread between its first and last whole-unit CTA end
+    spread = []
+    for s_ in set(sm.tolist()):
+        m = (sm == s_) & (slot >= 0) & (slot < a.w)
+        if m.sum() > 1:
+            spread.append((en[m].max() - en[m].min()) / 1e3)
+    spread = np.array(spread)
+    print(f"whole-unit CTAs of one SM: end spread us min {spread.min():.1f} median {np.median(spread):.1f} max {spread.max():.1f}")
