@@ -73,6 +73,9 @@ __device__ __forceinline__ void hmma(float d[4], uint32_t a0, uint32_t a1, uint3
 #else
 #define KVT_STAMP(k) do { } while (0)
 #endif
+#ifndef KVT_COLS
+#define KVT_COLS 1     // g <= 4: QK columns (head h hi, head h lo) adjacent, one softmax head per lane
+#endif
 #ifndef KVT_EXP
 #define KVT_EXP 0      // profiling experiments only: 1 = skip PV, 2 = skip QK, 3 = both, 4 = stream tiles only, 5 = no tail
 #endif
@@ -212,6 +215,11 @@ __device__ __forceinline__ void v_frag(const VRaw<VB>& r, int g4, uint32_t hA[4]
     }
 }
 
+// NC weight tile (g <= 4): the PV B operand of k-step ks, token pair j (tokens 16 ks + j, + 8) and head n is the word
+// wt_idx(ks, j, n) + group; o(j) = 4 (j & 1) + (j & 2) skews the heads so that the 8 lanes of every STS.128 (writer:
+// j = gid, n = tig) and every LDS.128 (reader: j = tig or tig + 4, n = gid) phase hit distinct 16-byte bank groups.
+__device__ __forceinline__ int wt_idx(int ks, int j, int n) { return ((ks * 8 + j) * 8 + ((n + 4 * (j & 1) + (j & 2)) & 7)) * 4; }
+
 // Output row writer: mode 0 bf16, 1 fp32 (o = O / L), 2 partial (m, l, o).
 __device__ __forceinline__ void write_row(const DecodeArgs& a, void* out, int mode, size_t row, int c, float M, float L,
                                           float O) {
@@ -288,6 +296,12 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
                                         const int tile_lo, const int tile_hi, const bool do_tail, const int cta,
                                         const int slot, const int c_first, const int count) {
     using Gm = Geo<KB, VB, GM>;
+    // NC (g <= 4): the 8 QK columns are (head 0 hi, head 0 lo, head 1 hi, ...), so a lane's two accumulator
+    // columns hold the hi and lo parts of ONE head (tig): the fold is one add, no shuffle, and each lane runs the
+    // softmax of one head (no duplicated work).  The weights go to the PV B tile as [ks][token pair][head][group]
+    // words, read back with one LDS.128 per (k-step, pair) — see `wt_idx`.
+    constexpr bool NC = (GM == 4) && KVT_COLS;
+    constexpr int JH = NC ? 1 : 2;                                         // softmax heads per lane
     float* q_s = reinterpret_cast<float*>(smem);                           // [GM][128]
     float* tail_s = reinterpret_cast<float*>(smem + Gm::Q_BYTES);          // [GM][2 + D]
     uint8_t* body = smem + Gm::Q_BYTES + Gm::TAIL_BYTES;
@@ -329,7 +343,7 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
     // ---- stage the tail rows [n_main, S) into shared memory with bulk copies (one round trip instead of a
     // dependent global load per token group); `tl` then addresses them with the cache's own indexing ----
     // softmax heads of this thread (the QK D columns it holds after the hi/lo fold)
-    const int hA = (GM == 8) ? 2 * tig : 2 * (tig & 1);
+    const int hA = (GM == 8) ? 2 * tig : (NC ? tig : 2 * (tig & 1));
     // ---- per-head power-of-two scale of q (max |q 2^qa| in [64, 128)), computed once per CTA ----
     float* qmax_s = tail_s;                               // tail_s is free until the tail is merged
     if (warp == 0) {
@@ -346,7 +360,7 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
     uint32_t q_h[16];
     float qa_inv[2];
     {
-        const int qh = (GM == 4) ? (gid & 3) : gid;
+        const int qh = (GM == 4) ? (NC ? (gid >> 1) : (gid & 3)) : gid;
         const int qa = 7 - frexp_e(qmax_s[qh]);
 #pragma unroll
         for (int m = 0; m < 16; ++m) {
@@ -359,13 +373,13 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
                                                q_s[qh * D + 32 * tig + KSlots<KB>::c1(m)] * sc));
         }
 #pragma unroll
-        for (int j = 0; j < 2; ++j) qa_inv[j] = pow2(24 - (7 - frexp_e(qmax_s[hA + j])));   // undoes 2^qa, 2^-24
+        for (int j = 0; j < JH; ++j) qa_inv[j] = pow2(24 - (7 - frexp_e(qmax_s[hA + j])));   // undoes 2^qa, 2^-24
     }
     // per-token keys: Q_g = sum of the head's q over group g (the zero-point term sum_g z_(t,g) Q_g)
     float qg[KPT ? 4 : 1][2];
     if constexpr (KPT) {
 #pragma unroll
-        for (int j = 0; j < 2; ++j)
+        for (int j = 0; j < JH; ++j)
 #pragma unroll
             for (int gg = 0; gg < 4; ++gg) {
                 float acc = 0.0f;
@@ -689,14 +703,14 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
             bz[0] += __shfl_xor_sync(kFull, bz[0], 8);
             bz[0] += __shfl_xor_sync(kFull, bz[0], 16);
             bias[0] = __shfl_sync(kFull, bz[0], hA);
-            bias[1] = __shfl_sync(kFull, bz[0], hA + 1);
+            if constexpr (!NC) bias[1] = __shfl_sync(kFull, bz[0], hA + 1);
         }
         __syncwarp();
         // (2) B operand of QK: q_h * s_h split exactly into hi + lo
         uint32_t bq[16], bq_lo[(GM == 8 && !KPT) ? 16 : 1];
         if constexpr (KPT) {
 #pragma unroll
-            for (int m = 0; m < 16; ++m) bq[m] = q_h[m];   // q (bf16) is exact in fp16: no lo half (GM = 4: the
+            for (int m = 0; m < 16; ++m) bq[m] = (NC && (gid & 1)) ? 0u : q_h[m];   // q (bf16) is exact in fp16: no lo half (NC: the odd columns are 0; else GM = 4: the
                                                             // 8 columns hold heads gid & 3, i.e. the 4 heads twice)
         } else {
             const uint4* shv = reinterpret_cast<const uint4*>(sh_s + tig * Gm::SH_STRIDE);
@@ -713,7 +727,7 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
                         bq[m] = h2u(hi);
                         bq_lo[m] = h2u(__hfma2(u2h(q_h[m]), u2h(sv[e]), __hneg2(hi)));
                     } else {
-                        bq[m] = (gid >= 4) ? h2u(__hfma2(u2h(q_h[m]), u2h(sv[e]), __hneg2(hi))) : h2u(hi);
+                        bq[m] = (NC ? (gid & 1) : (gid >= 4)) ? h2u(__hfma2(u2h(q_h[m]), u2h(sv[e]), __hneg2(hi))) : h2u(hi);
                     }
                 }
             }
@@ -755,10 +769,10 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
 #pragma unroll
                 for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) {
+                    for (int i = 0; i < 4; i += (NC ? 2 : 1)) {     // NC: column 2 tig + 1 is zero
                         const uint32_t mw = mk[mt][i >> 1][gg];
-                        dq[mt][i] = fmaf(bf2f(mw & 0xffffu) * qa_inv[i & 1], acc[mt][i],
-                                         fmaf(bf2f(mw >> 16), qg[gg][i & 1], dq[mt][i]));
+                        dq[mt][i] = fmaf(bf2f(mw & 0xffffu) * qa_inv[NC ? 0 : (i & 1)], acc[mt][i],
+                                         fmaf(bf2f(mw >> 16), qg[gg][NC ? 0 : (i & 1)], dq[mt][i]));
                     }
             }
         } else if (KVT_EXP != 2 && KVT_EXP != 3) {
@@ -794,19 +808,25 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
                 }
             }
 #pragma unroll
-            for (int mt = 0; mt < 2; ++mt)
+            for (int mt = 0; mt < 2; ++mt) {
+                if constexpr (NC) {                   // (hi + lo) of head tig, rows gid and gid + 8
+                    dq[mt][0] = (de[mt][0] + dd[mt][0]) + (de[mt][1] + dd[mt][1]);
+                    dq[mt][2] = (de[mt][2] + dd[mt][2]) + (de[mt][3] + dd[mt][3]);
+                } else {
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    dq[mt][i] = de[mt][i] + dd[mt][i];
-                    if constexpr (GM == 4) dq[mt][i] += __shfl_xor_sync(kFull, dq[mt][i], 2);
+                    for (int i = 0; i < 4; ++i) {
+                        dq[mt][i] = de[mt][i] + dd[mt][i];
+                        if constexpr (GM == 4) dq[mt][i] += __shfl_xor_sync(kFull, dq[mt][i], 2);
+                    }
                 }
+            }
         }
         // (4) logits (log2 domain) for tokens {16mt + gid + 8r} x heads {hA, hA + 1}; online softmax with a
         // lazy reference max: it only moves when the tile max exceeds it by more than 8 (so p <= 2^8)
         float alpha[2], p[2][2][2];        // p[mt][r][j]
         bool resc = false;
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
+        for (int j = 0; j < JH; ++j) {
             const float cs = KPT ? a.scale_log2 : a.scale_log2 * qa_inv[j] * ks_inv;   // KPT: dq holds q.k
             const float cb = KPT ? 0.0f : a.scale_log2 * bias[j];
             float l4[4];
@@ -837,7 +857,46 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
         }
         // (5) value weights w = p * s_v * 2^kp (fp16 pairs (T, T+8)) and zero sums p * z_v
         float kfac = 1.0f;
-        {
+        if constexpr (NC) {
+            // head tig, this lane's 4 tokens x all 4 value groups
+            uint32_t mw[2][2][4];
+            uint32_t smb = 0;
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    const uint4 m4 = *reinterpret_cast<const uint4*>(vm_s + (16 * mt + gid + 8 * r) * 4);
+                    mw[mt][r][0] = m4.x; mw[mt][r][1] = m4.y; mw[mt][r][2] = m4.z; mw[mt][r][3] = m4.w;
+                    smb = __vmaxu2(__vmaxu2(smb, __vmaxu2(m4.x, m4.y)), __vmaxu2(m4.z, m4.w));   // per-halfword max
+                }
+            smb &= 0xffffu;                                       // the scale halves
+            smb = __reduce_max_sync(kFull, smb);
+            const int kt = 7 - frexp_e(bf2f(smb));
+            if (kt < kp) {
+                if (it > 0) { kfac = pow2(kt - kp < -126 ? -126 : kt - kp); resc = true; }
+                kp = kt;
+            }
+            const float ksc = pow2(kp);
+            uint32_t wv[2][4];
+#pragma unroll
+            for (int gr = 0; gr < 4; ++gr) {
+                float2 za = zacc2[gr][0];
+                if (resc) za = dec::fmul2(za, make_float2(alpha[0], alpha[0]));
+#pragma unroll
+                for (int mt = 0; mt < 2; ++mt) {
+                    const uint32_t w0 = mw[mt][0][gr], w1 = mw[mt][1][gr];
+                    const float2 sv = dec::fmul2(make_float2(bf2f(w0 & 0xffffu), bf2f(w1 & 0xffffu)), make_float2(ksc, ksc));
+                    const float2 wa = dec::fmul2(make_float2(p[mt][0][0], p[mt][1][0]), sv);
+                    wv[mt][gr] = h2u(__floats2half2_rn(wa.x, wa.y));
+                    const float2 zz = make_float2(__uint_as_float(w0 & 0xffff0000u), __uint_as_float(w1 & 0xffff0000u));
+                    za = dec::ffma2(make_float2(p[mt][0][0], p[mt][1][0]), zz, za);
+                }
+                zacc2[gr][0] = za;
+            }
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+                *reinterpret_cast<uint4*>(w_s + wt_idx(mt, gid, tig)) = make_uint4(wv[mt][0], wv[mt][1], wv[mt][2], wv[mt][3]);
+        } else        {
             // meta words of this lane's 4 tokens x its value groups (GM == 4: the tig pair splits the groups)
             uint32_t mw[2][2][NGL];
             uint32_t smb = 0;
@@ -900,7 +959,9 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
         // (6) PV on the tensor cores: 8 m-tiles (γ, μ) x 2 k-steps of 16 tokens
         if (KVT_EXP != 1 && KVT_EXP != 3) {
             if (__any_sync(kFull, resc)) {
-                const float r0 = alpha[0] * kfac, r1 = alpha[1] * kfac;   // PV columns 2tig, 2tig+1
+                // PV columns 2tig, 2tig+1 = heads 2tig, 2tig+1; NC: their softmax state lives in lanes tig' = 2tig (+1)
+                const float r0 = (NC ? __shfl_sync(kFull, alpha[0], (lane & ~3) | ((2 * tig) & 3)) : alpha[0]) * kfac;
+                const float r1 = (NC ? __shfl_sync(kFull, alpha[0], (lane & ~3) | ((2 * tig + 1) & 3)) : alpha[1]) * kfac;
 #pragma unroll
                 for (int i = 0; i < 8; ++i) { o[i][0] *= r0; o[i][1] *= r1; o[i][2] *= r0; o[i][3] *= r1; }
             }
@@ -908,10 +969,21 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
             for (int ks = 0; ks < 2; ++ks) {
                 VRaw<VB> raw;
                 v_load<VB>(vc_s, ks, tig, gid, raw);
+                uint4 B0 = make_uint4(0, 0, 0, 0), B1 = B0;
+                if constexpr (NC) {                 // all 4 groups' weights of pairs tig, tig + 4, head gid
+                    B0 = *reinterpret_cast<const uint4*>(w_s + wt_idx(ks, tig, gid));
+                    B1 = *reinterpret_cast<const uint4*>(w_s + wt_idx(ks, tig + 4, gid));
+                }
 #pragma unroll
                 for (int gam = 0; gam < 4; ++gam) {
-                    const uint32_t* wr = w_s + (gam * 2 + ks) * 64 + 4 * (gam >> 1) + gid;
-                    const uint32_t b0 = wr[tig * 8], b1 = wr[(tig + 4) * 8];
+                    uint32_t b0, b1;
+                    if constexpr (NC) {
+                        b0 = gam == 0 ? B0.x : (gam == 1 ? B0.y : (gam == 2 ? B0.z : B0.w));
+                        b1 = gam == 0 ? B1.x : (gam == 1 ? B1.y : (gam == 2 ? B1.z : B1.w));
+                    } else {
+                        const uint32_t* wr = w_s + (gam * 2 + ks) * 64 + 4 * (gam >> 1) + gid;
+                        b0 = wr[tig * 8]; b1 = wr[(tig + 4) * 8];
+                    }
                     uint32_t hA4[4], hB4[4];
                     v_frag<VB>(raw, gam, hA4, hB4);
                     hmma(o[2 * gam], hA4[0], hA4[1], hB4[0], hB4[1], b0, b1);
@@ -930,12 +1002,33 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
     }
     // ---- warp epilogue: l over the 8 row-groups, zero sums, o = D * 2^(24 - P(row) - kp) + zacc ----
     float zacc[4][2];
+    if constexpr (NC) {
+        // lane (gid, tig): softmax state of head tig; the PV owner lanes (tig < 2) need heads 2tig, 2tig + 1
+        float z[4], l = l_part[0];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) z[i] = zacc2[i][0].x + zacc2[i][0].y;
+#pragma unroll
+        for (int off = 4; off <= 16; off <<= 1) {
+            l += __shfl_xor_sync(kFull, l, off);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) z[i] += __shfl_xor_sync(kFull, z[i], off);
+        }
+        const float m0 = m_run[0];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int src = (lane & ~3) | ((2 * tig + j) & 3);
+            m_run[j] = __shfl_sync(kFull, m0, src);
+            l_part[j] = __shfl_sync(kFull, l, src);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) zacc[i][j] = __shfl_sync(kFull, z[i], src);
+        }
+    }
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) zacc[i][j] = zacc2[i][j].x + zacc2[i][j].y;
+        for (int j = 0; j < 2; ++j) if (!NC) zacc[i][j] = zacc2[i][j].x + zacc2[i][j].y;
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
+    for (int j = 0; j < (NC ? 0 : 2); ++j) {
         float l = (GM == 8 || tig < 2) ? l_part[j] : 0.0f;
         l += __shfl_xor_sync(kFull, l, 4);
         l += __shfl_xor_sync(kFull, l, 8);
@@ -950,7 +1043,7 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
             zacc[gam][j] = z;
         }
     }
-    if constexpr (GM == 4) {   // tig 0/1 hold groups 0,1 of heads (0,1)/(2,3) in slots 0,1; tig 2/3 groups 2,3
+    if constexpr (GM == 4 && !NC) {   // tig 0/1 hold groups 0,1 of heads (0,1)/(2,3) in slots 0,1; tig 2/3 groups 2,3
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
             zacc[2][j] = __shfl_xor_sync(kFull, zacc[0][j], 2);
