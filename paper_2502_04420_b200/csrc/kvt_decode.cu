@@ -260,8 +260,8 @@ int32_t launch_decode(const Geometry& g, const CachePtrs& c, const uint16_t* q, 
         a.n_cta = n;
         a.trace = nullptr;
 #if KVT_TRACE
-        if (!g_trace) { cudaMalloc(&g_trace, sizeof(unsigned long long) * 11 * 4096); }
-        cudaMemsetAsync(g_trace, 0, sizeof(unsigned long long) * 11 * 4096, (cudaStream_t)stream);
+        if (!g_trace) { cudaMalloc(&g_trace, sizeof(unsigned long long) * 15 * 4096); }
+        cudaMemsetAsync(g_trace, 0, sizeof(unsigned long long) * 15 * 4096, (cudaStream_t)stream);
         a.trace = g_trace;
 #endif
         // programmatic dependent launch: the kernel's prologue (length scan, q setup) may overlap the tail of
@@ -331,6 +331,6 @@ int32_t launch_combine(const float* parts, int n_parts, int B, int H_q, int d, v
 
 #if KVT_TRACE
 extern "C" int32_t kvt_debug_trace(unsigned long long* host, int32_t n) {
-    return g_trace && cudaMemcpy(host, g_trace, sizeof(unsigned long long) * 11 * 4096, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 8;
+    return g_trace && cudaMemcpy(host, g_trace, sizeof(unsigned long long) * 15 * 4096, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 8;
 }
 #endif

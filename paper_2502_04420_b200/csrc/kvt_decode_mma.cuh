@@ -995,6 +995,14 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
     }
 
     KVT_STAMP(2);
+#if KVT_TRACE
+    if (a.trace && lane == 0 && blockIdx.x < 4096) {        // per-warp end of the tile loop (first segment)
+        unsigned long long t_;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+        unsigned long long* p_ = a.trace + 11 * 4096 + 4 * blockIdx.x + warp;
+        if (*p_ == 0ull) *p_ = t_;
+    }
+#endif
     __syncwarp();
     if (lane == 0) {
 #pragma unroll

@@ -41,13 +41,14 @@ for _ in range(5):
     flush.zero_()
     kvt.decode_attention(cache, q, sl, scale=1 / math.sqrt(128), workspace=ws)
 torch.cuda.synchronize()
-buf = (ctypes.c_ulonglong * (11 * 4096))()
+buf = (ctypes.c_ulonglong * (15 * 4096))()
 assert kmod._lib.kvt_debug_trace(buf, 4096) == 0
 allb = np.frombuffer(buf, dtype=np.uint64).astype(np.int64)
 t = allb[:3 * 4096].reshape(4096, 3)
-st4 = allb[3 * 4096:].reshape(4096, 8)
+st4 = allb[3 * 4096:11 * 4096].reshape(4096, 8)
+wend = allb[11 * 4096:15 * 4096].reshape(4096, 4)
 keep = t[:, 2] > 0
-t, st4 = t[keep], st4[keep]
+t, st4, wend = t[keep], st4[keep], wend[keep]
 t0 = t[:, 1].min()
 if (st4[:, 0] > 0).all():
     ph = lambda a_, b_: (st4[:, b_] - st4[:, a_]) / 1e3
@@ -93,3 +94,9 @@ if (item >= 0).any():
             spread.append((en[m].max() - en[m].min()) / 1e3)
     spread = np.array(spread)
     print(f"whole-unit CTAs of one SM: end spread us min {spread.min():.1f} median {np.median(spread):.1f} max {spread.max():.1f}")
+
+if (wend > 0).all():
+    sp = (wend.max(axis=1) - wend.min(axis=1)) / 1e3
+    fromend = (t[:, 2] - wend.max(axis=1)) / 1e3
+    print(f"per-CTA spread of its 4 warps' loop ends (us): min {sp.min():.1f} p10 {np.percentile(sp, 10):.1f} median {np.median(sp):.1f}"
+          f" p90 {np.percentile(sp, 90):.1f} max {sp.max():.1f};  last warp's loop end -> CTA end: median {np.median(fromend):.1f}")
