@@ -77,7 +77,8 @@ __device__ __forceinline__ void hmma(float d[4], uint32_t a0, uint32_t a1, uint3
 #define KVT_COLS 1     // g <= 4: QK columns (head h hi, head h lo) adjacent, one softmax head per lane
 #endif
 #ifndef KVT_EXP
-#define KVT_EXP 0      // profiling experiments only: 1 = skip PV, 2 = skip QK, 3 = both, 4 = stream tiles only, 5 = no tail
+#define KVT_EXP 0      // profiling experiments only: 1 = skip PV, 2 = skip QK, 3 = both, 4 = stream tiles only, 5 = no tail,
+                       // 6 = PV operands staged to shared memory instead of HMMA (tcgen05 cost probe)
 #endif
 // 2^x on the SFU (MUFU.EX2, flush-to-zero). exp2f adds a subnormal range fix-up (~4 more instructions) that
 // softmax does not need: every argument here is <= 8 and results below 2^-126 are negligible against l >= 1.
@@ -986,8 +987,18 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
                     }
                     uint32_t hA4[4], hB4[4];
                     v_frag<VB>(raw, gam, hA4, hB4);
-                    hmma(o[2 * gam], hA4[0], hA4[1], hB4[0], hB4[1], b0, b1);
-                    hmma(o[2 * gam + 1], hA4[2], hA4[3], hB4[2], hB4[3], b0, b1);
+                    if constexpr (KVT_EXP == 6) {
+                        // tcgen05 cost probe: the PV A operand (128 channels x 16 tokens fp16 = 4 KB per k-step) staged
+                        // to shared memory as a tcgen05.mma would need it, instead of feeding HMMA from registers
+                        // (the stores go to a small scratch: only the issue cost counts)
+                        const uint32_t st = smem_u32(sh_s) + (lane & 3) * 32;
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(st), "r"(hA4[0]), "r"(hA4[1]), "r"(hB4[0]), "r"(hB4[1]) : "memory");
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(st + 16), "r"(hA4[2]), "r"(hA4[3]), "r"(hB4[2]), "r"(hB4[3]) : "memory");
+                        (void)b0; (void)b1;      // tcgen05 would read the weight tile (B) from shared memory itself
+                    } else {
+                        hmma(o[2 * gam], hA4[0], hA4[1], hB4[0], hB4[1], b0, b1);
+                        hmma(o[2 * gam + 1], hA4[2], hA4[3], hB4[2], hB4[3], b0, b1);
+                    }
                 }
             }
         }
