@@ -45,9 +45,25 @@ constexpr int kTile = 32;
 constexpr int kWarps = 4;
 constexpr int kThreads = 128;
 
+// an opaque copy: the compiler keeps the value in a register instead of re-deriving it from %tid inside the tile loop
+__device__ __forceinline__ int opaque(int x) {
+    int y;
+    asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
+    return y;
+}
 __device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
 __device__ __forceinline__ __half2 u2h(uint32_t u) { return *reinterpret_cast<__half2*>(&u); }
 
+// D = A B (zero accumulator: the MMA reads RZ, no register moves to clear a chain's accumulator)
+__device__ __forceinline__ void hmma0(float d[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                      uint32_t b1) {
+    const float z = 0.0f;
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%10,%10,%10,%10};\n"
+        : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1), "f"(z));
+}
 __device__ __forceinline__ void hmma(float d[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
                                      uint32_t b1) {
     asm volatile(
@@ -309,8 +325,8 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
     const Geometry& g = a.g;
     // warp index through a lane-0 shuffle: the compiler then knows it is warp-uniform, so the per-warp TMA
     // addresses live in uniform registers (no per-copy R2UR broadcast loop around UBLKCP)
-    const int tid = threadIdx.x, lane = tid & 31, warp = __shfl_sync(kFull, tid >> 5, 0);
-    const int gid = lane >> 2, tig = lane & 3;
+    const int tid = threadIdx.x, lane = opaque(tid & 31), warp = __shfl_sync(kFull, tid >> 5, 0);
+    const int gid = opaque(lane >> 2), tig = opaque(lane & 3);
     const int gq = a.gq;
     const int S = a.seq_len[b];
     KVT_STAMP(0);
@@ -340,7 +356,7 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
     const int nqK = nq_key(g.mode, g.kb, g.G, g.R, S);
     const int nqV = nq_per_token(g.vb, g.R, S);
     const int n_main = ((nqK < nqV ? nqK : nqV) / kTile) * kTile;
-    const int n_my = tile_hi - tile_lo - warp > 0 ? (tile_hi - tile_lo - warp + kWarps - 1) / kWarps : 0;
+    const int n_my = opaque(tile_hi - tile_lo - warp > 0 ? (tile_hi - tile_lo - warp + kWarps - 1) / kWarps : 0);
     // ---- stage the tail rows [n_main, S) into shared memory with bulk copies (one round trip instead of a
     // dependent global load per token group); `tl` then addresses them with the cache's own indexing ----
     // softmax heads of this thread (the QK D columns it holds after the hi/lo fold)
@@ -794,17 +810,14 @@ __device__ __forceinline__ void segment(const DecodeArgs& a, uint8_t* smem, cons
             }
             float de[2][4], dd[2][4];
 #pragma unroll
-            for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-                for (int i = 0; i < 4; ++i) de[mt][i] = dd[mt][i] = 0.0f;
-#pragma unroll
             for (int s = 0; s < 8; ++s) {
 #pragma unroll
                 for (int mt = 0; mt < 2; ++mt) {
                     float* acc = (s & 1) ? dd[mt] : de[mt];
                     const uint32_t a0 = k_slot<KB>(w[2 * mt], 2 * s), a1 = k_slot<KB>(w[2 * mt + 1], 2 * s);
                     const uint32_t a2 = k_slot<KB>(w[2 * mt], 2 * s + 1), a3 = k_slot<KB>(w[2 * mt + 1], 2 * s + 1);
-                    hmma(acc, a0, a1, a2, a3, bq[2 * s], bq[2 * s + 1]);
+                    if (s < 2) hmma0(acc, a0, a1, a2, a3, bq[2 * s], bq[2 * s + 1]);   // chain starts
+                    else hmma(acc, a0, a1, a2, a3, bq[2 * s], bq[2 * s + 1]);
                     if constexpr (GM == 8) hmma(acc, a0, a1, a2, a3, bq_lo[2 * s], bq_lo[2 * s + 1]);
                 }
             }
