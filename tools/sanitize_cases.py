@@ -1,6 +1,6 @@
 """Small-shape invocations of every kernel path for compute-sanitizer:
     compute-sanitizer --tool memcheck|racecheck|synccheck python tools/sanitize_cases.py
-tensor-core decode (whole units, stream-K cut with the fused last-CTA merge, staged tail, paged records, per-token
+tensor-core decode (per-SM plan, whole units, stream-K cut with the fused last-CTA merge, staged tail, paged records, per-token
 keys, g = 7), the fused append -> decode launch (PDL prologue), the partial push, the generic CUDA-core kernel +
 combine, K1 append (prefill and one-token), K5 sensitivity."""
 import math
@@ -78,6 +78,12 @@ def sens():
         kvt.layer_sensitivity(mode, 32, R, Q, K, V, 112, [(4, 2), (8, 8)])
 
 
+if os.environ.get("KVT_SAN_ONLY") == "smplan":
+    run("mma per-SM plan (B=48: 2 whole units + a piece per SM)", lambda: decode(kvt.LayerSpec.kivi(4, 2), 48, 8, 4,
+        kvt_synth.ragged_lengths(48, 1, 200, seed=61).tolist(), 61))
+    sys.exit(0)
+run("mma per-SM plan (B=48: 2 whole units + a piece per SM)", lambda: decode(kvt.LayerSpec.kivi(4, 2), 48, 8, 4,
+    kvt_synth.ragged_lengths(48, 1, 200, seed=61).tolist(), 61))
 run("mma whole units (ragged, staged tail)", lambda: decode(kvt.LayerSpec.kivi(4, 2), 3, 2, 4, [100, 700, 33], 1))
 run("mma stream-K cut + fused merge", lambda: decode(kvt.LayerSpec.kivi(4, 2), 2, 1, 4, [4096, 3000], 3))
 run("mma paged", lambda: decode(kvt.LayerSpec.kivi(4, 4), 3, 2, 4, [100, 700, 33], 5, paged=True))
