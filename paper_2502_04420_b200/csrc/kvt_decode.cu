@@ -270,9 +270,10 @@ int32_t launch_decode(const Geometry& g, const CachePtrs& c, const uint16_t* q, 
         // Only when the grid (nearly) fills the wave: CTAs dispatched while the append still occupies SMs are
         // placed unevenly, which a partial wave cannot absorb (Qwen, 256 whole units on 444 slots: 15 449
         // tokens/s with PDL vs 19 583 without; Llama, 512 on 592: +2% with PDL).
-        static const bool pdl_env = [] { const char* e = getenv("KVT_PDL"); return !e || atoi(e) != 0; }();
+        // KVT_PDL: 0 = never, unset/1 = the rule below, 2 = also with the per-SM plan (A/B only)
+        static const int pdl_env = [] { const char* e = getenv("KVT_PDL"); return e ? atoi(e) : 1; }();
         // Not with the per-SM plan either: llama-3.25 step 4.606 ms without PDL vs 4.682 ms with it (B = 64).
-        const bool pdl = pdl_env && 4LL * n >= 3LL * in.occ * sms && w == 0;
+        const bool pdl = pdl_env != 0 && 4LL * n >= 3LL * in.occ * sms && (w == 0 || pdl_env == 2);
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(n);
         cfg.blockDim = dim3(kThreads);
