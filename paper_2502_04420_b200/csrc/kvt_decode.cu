@@ -169,13 +169,14 @@ static size_t sched_bytes(const Geometry& g, int sms) {
 // (Qwen g = 7: one whole unit + a piece on 3-CTA SMs) it lost (K4V4 106 -> 113 us): once the piece is done the
 // whole unit runs alone on its SM with 4 warps, which cannot keep the SM busy.
 static int plan_sm_w(const Geometry& g, int occ, int sms) {
-    static const bool on = [] { const char* e = getenv("KVT_SMPLAN"); return !e || atoi(e) != 0; }();   // A/B switch
+    // A/B switch: 0 = off, unset/1 = the rule below, 2 = also w = 1
+    static const int on = [] { const char* e = getenv("KVT_SMPLAN"); return e ? atoi(e) : 1; }();
     if (!on) return 0;
     const long long units = (long long)g.B * g.H, slots = (long long)occ * sms;
     const long long per_sm = (units + sms - 1) / sms;
     const bool whole = units <= slots && 2 * units >= 3LL * sms && 5 * per_sm * sms <= 6 * units;   // plan_ctas' rule
     const long long w = units / sms;
-    if (!whole || w < 2 || w + 1 > occ || units % sms == 0) return 0;
+    if (!whole || w < (on == 2 ? 1 : 2) || w + 1 > occ || units % sms == 0) return 0;
     return (int)w;
 }
 
