@@ -200,7 +200,12 @@ __device__ void per_channel_key(int phase, int bits, int G, int F, int L0, int S
     }
 }
 
-__global__ void __launch_bounds__(kWarps * 32) append_kernel(AppendArgs a) {
+// One instance per key mode.  KIVI (per-channel keys) is bounded to 8 CTAs per SM (64 registers): its prefill is
+// bound by global-load latency (ncu: long-scoreboard stalls first, 16 warps per SM at 128 registers), and twice
+// the warps hide it — B = 64, 8k: K4V2 1.46 -> 1.24 ms, K2V2 1.43 -> 1.23 ms (KV8 1.65 -> 1.67).  The per-token
+// instance keeps 4 CTAs per SM (128 registers; bounded to 8 it ran 15% slower, unbounded (140) 20% slower).
+template <bool KPC>
+__global__ void __launch_bounds__(kWarps * 32, KPC ? 8 : 4) append_kernel(AppendArgs a) {
     // the decode attention launched next may start its q/length prologue now (it waits for this grid's
     // completion before reading the cache: griddepcontrol.wait in decode_mma_kernel)
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
@@ -229,14 +234,14 @@ __global__ void __launch_bounds__(kWarps * 32) append_kernel(AppendArgs a) {
 
     // phase 0 (chunk 0): residual-sourced groups; phase 1: input-sourced groups (everyone)
     if (chunk == 0) {
-        if (g.key_per_channel)
+        if (KPC)
             per_channel_key(0, g.kb, g.G, g.F, L0, S, kin, a.s2, kc, g.row_k, km, kr, warp, kWarps, lane, g.rec, g.rec_km, bt, pstride);
         else
             per_token_tensor(0, g.kb, g.G, g.R, L0, S, kin, a.s2, kd, kr, warp, kWarps, lane);
         per_token_tensor(0, g.vb, g.G, g.R, L0, S, vin, a.s2, vd, vr, warp, kWarps, lane);
     }
     const int wid = chunk * kWarps + warp, nw = gridDim.x * kWarps;
-    if (g.key_per_channel)
+    if (KPC)
         per_channel_key(1, g.kb, g.G, g.F, L0, S, kin, a.s2, kc, g.row_k, km, kr, wid, nw, lane, g.rec, g.rec_km, bt, pstride);
     else
         per_token_tensor(1, g.kb, g.G, g.R, L0, S, kin, a.s2, kd, kr, wid, nw, lane);
@@ -244,7 +249,7 @@ __global__ void __launch_bounds__(kWarps * 32) append_kernel(AppendArgs a) {
     // phase 2 (chunk 0): new residual tokens, after every residual read of phase 0
     if (chunk == 0) {
         __syncthreads();
-        if (g.key_per_channel)
+        if (KPC)
             per_channel_key(2, g.kb, g.G, g.F, L0, S, kin, a.s2, kc, g.row_k, km, kr, warp, kWarps, lane, g.rec, g.rec_km, bt, pstride);
         else
             per_token_tensor(2, g.kb, g.G, g.R, L0, S, kin, a.s2, kd, kr, warp, kWarps, lane);
@@ -266,7 +271,8 @@ int32_t launch_append(const Geometry& g, const CachePtrs& c, const uint16_t* k_n
     if (chunks > 4096) chunks = 4096;
     if (g.B > 65535 || g.H > 65535) return fail(KVT_ERR_UNSUPPORTED, "append: batch/heads exceed grid limits");
     dim3 grid(chunks, g.H, g.B);
-    append_kernel<<<grid, kWarps * 32, 0, (cudaStream_t)stream>>>(a);
+    if (g.key_per_channel) append_kernel<true><<<grid, kWarps * 32, 0, (cudaStream_t)stream>>>(a);
+    else append_kernel<false><<<grid, kWarps * 32, 0, (cudaStream_t)stream>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(KVT_ERR_CUDA, "append launch: %s", cudaGetErrorString(e));
     return KVT_OK;
