@@ -607,8 +607,17 @@ def run_kvt(args):
                  for i in range(args.steps)) / args.steps
         e = by_pair.setdefault(key, {"layers": 0, "us": 0.0, "bytes": 0.0})
         e["layers"] += 1; e["us"] += t * 1000.0; e["bytes"] += nb
+    plans = {}
+    for l, s in enumerate(specs):
+        key = f"{'PT' if s.mode != 1 else ''}K{s.key_bits}V{s.value_bits}"
+        if key not in plans:
+            try:
+                plans[key] = kvt.decode_plan(caches[l], Hq)          # the work plan of the launch (kvt_decode_plan)
+            except Exception as e:                                 # noqa: BLE001 - reporting only
+                plans[key] = {"error": str(e)}
     roofline["by_pair"] = {k: {"layers": v["layers"], "us_per_launch": v["us"] / v["layers"],
-                               "frac": v["bytes"] / (v["us"] / 1e6) / 1e9 / peak} for k, v in by_pair.items()}
+                               "frac": v["bytes"] / (v["us"] / 1e6) / 1e9 / peak, "plan": plans.get(k)}
+                           for k, v in by_pair.items()}
 
     # ---- e2e: host (pinned) inputs -> device, step, outputs -> host, every step ----
     e2e = None

@@ -31,7 +31,8 @@
 extern "C" {
 #endif
 
-#define KVT_ABI_VERSION 3u   /* 3: kvt_append_decode_attention; merge counters first in the workspace */
+#define KVT_ABI_VERSION 4u   /* 3: kvt_append_decode_attention; merge counters first in the workspace;
+                                4: schedule counters after them (per-SM plan), kvt_decode_plan */
 
 typedef enum {
     KVT_OK = 0,
@@ -167,6 +168,11 @@ int32_t kvt_quantize_append(const kvt_layer_cache* cache, const void* k_new, con
  * anything, so the call is ordered after every preceding stream operation like a plain launch. */
 int32_t kvt_decode_workspace_bytes(const kvt_layer_cache* cache, int32_t n_q_heads,
                                    const int32_t* seq_len_host, uint64_t* bytes);
+/* The work plan kvt_decode_attention would use for this cache (same arguments as kvt_decode_workspace_bytes):
+ * out[0] = kernel (1 tensor-core tile-record kernel, 0 generic CUDA-core kernel), out[1] = CTAs launched (generic:
+ * KV splits), out[2] = whole units per SM of the per-SM plan (0: stream-K / whole units by CTA index),
+ * out[3] = resident CTAs per SM of the instance.  Needs a CUDA device (occupancy query); host only, no launch. */
+int32_t kvt_decode_plan(const kvt_layer_cache* cache, int32_t n_q_heads, const int32_t* seq_len_host, int32_t out[4]);
 int32_t kvt_decode_attention(const kvt_layer_cache* cache, const void* q, int32_t n_q_heads,
                              const int32_t* seq_len_host, const int32_t* seq_len_dev,
                              float softmax_scale, void* out, int32_t out_dtype,

@@ -209,6 +209,18 @@ extern "C" int32_t kvt_decode_workspace_bytes(const kvt_layer_cache* cache, int3
     return KVT_OK;
 }
 
+extern "C" int32_t kvt_decode_plan(const kvt_layer_cache* cache, int32_t H_q, const int32_t* seq_len_host, int32_t out[4]) {
+    clear_error();
+    if (!out) return fail(KVT_ERR_INVALID_ARG, "null out");
+    Geometry g; CachePtrs p;
+    int32_t st = cache_geometry(cache, &g, &p);
+    if (st) return st;
+    if (H_q <= 0 || H_q % g.H != 0 || H_q / g.H > 8) return fail(KVT_ERR_INVALID_ARG, "n_q_heads must be 1..8 x kv_heads");
+    int plan = g.cap;
+    if (seq_len_host) { plan = 0; for (int b = 0; b < g.B; ++b) plan = seq_len_host[b] > plan ? seq_len_host[b] : plan; }
+    return decode_plan(g, H_q, plan, out);
+}
+
 extern "C" int32_t kvt_decode_attention(const kvt_layer_cache* cache, const void* q, int32_t H_q,
                                         const int32_t* seq_len_host, const int32_t* seq_len_dev, float scale,
                                         void* out, int32_t out_dtype, void* ws, uint64_t ws_bytes, void* stream) {

@@ -215,6 +215,23 @@ size_t decode_workspace(const Geometry& g, int H_q, int plan_len) {
     return ns > 1 ? counters_bytes(g) + sched_bytes(g, sms) + parts_bytes(ns, g.B, H_q) : 0;
 }
 
+int32_t decode_plan(const Geometry& g, int H_q, int plan_len, int32_t out[4]) {
+    using namespace dec;
+    const int GM = (H_q / g.H) <= 4 ? 4 : 8;
+    Instance in; int sms = 148;
+    const int kind = kernel_kind(g);
+    int32_t st = get_instance(g.kb, g.vb, kind, GM, &in, &sms);
+    if (st) return st;
+    if (kind >= 2) {
+        const int w = plan_sm_w(g, in.occ, sms);
+        out[0] = 1; out[1] = w ? in.occ * sms : plan_ctas(g, plan_len, in.occ, sms); out[2] = w;
+    } else {
+        out[0] = 0; out[1] = plan_splits(g, plan_len, in.occ, sms); out[2] = 0;
+    }
+    out[3] = in.occ;
+    return KVT_OK;
+}
+
 int32_t launch_decode(const Geometry& g, const CachePtrs& c, const uint16_t* q, int H_q, const int32_t* seq_len,
                       int plan_len, float scale, void* out, int out_mode, void* workspace, size_t ws_bytes,
                       void* stream, float* const* push, int n_push, bool early) {

@@ -80,6 +80,7 @@ int32_t launch_decode(const Geometry& g, const CachePtrs& c, const uint16_t* q, 
                       void* workspace, size_t ws_bytes, void* stream, float* const* push = nullptr, int n_push = 0,
                       bool early = false);
 size_t decode_workspace(const Geometry& g, int H_q, int plan_len);
+int32_t decode_plan(const Geometry& g, int H_q, int plan_len, int32_t out[4]);
 int32_t launch_combine(const float* parts, int n_parts, int B, int H_q, int d, void* out, int out_dtype,
                        void* stream);
 int32_t launch_sensitivity(int mode, int G, int R, const uint16_t* q, int H_q, int T_q, int q_pos0,

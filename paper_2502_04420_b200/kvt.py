@@ -71,6 +71,7 @@ def _load():
         "kvt_quantize_append": (i32, [ctypes.POINTER(_Cache), P, P, ctypes.POINTER(ctypes.c_int64), P, P, P, P,
                                       i32, P]),
         "kvt_decode_workspace_bytes": (i32, [ctypes.POINTER(_Cache), i32, P, ctypes.POINTER(u64)]),
+        "kvt_decode_plan": (i32, [ctypes.POINTER(_Cache), i32, P, ctypes.POINTER(i32)]),
         "kvt_decode_attention": (i32, [ctypes.POINTER(_Cache), P, i32, P, P, ctypes.c_float, P, i32, P, u64, P]),
         "kvt_append_decode_attention": (i32, [ctypes.POINTER(_Cache), P, P, ctypes.POINTER(ctypes.c_int64), P, P, i32,
                                               P, i32, P, ctypes.c_float, P, i32, P, u64, P]),
@@ -104,7 +105,7 @@ EXPORTED = ("kvt_abi_version", "kvt_status_string", "kvt_last_error", "kvt_confi
             "kvt_decode_workspace_bytes", "kvt_decode_attention", "kvt_decode_attention_partial",
             "kvt_combine_partials", "kvt_sensitivity_workspace_bytes", "kvt_layer_sensitivity",
             "kvt_pareto_prune", "kvt_dbscan", "kvt_prune_and_cluster", "kvt_search_space_log10", "kvt_page_bytes",
-            "kvt_decode_attention_partial_push", "kvt_append_decode_attention")
+            "kvt_decode_attention_partial_push", "kvt_append_decode_attention", "kvt_decode_plan")
 
 
 def lib():
@@ -307,6 +308,15 @@ def quantize_append(cache: LayerCache, k_new: torch.Tensor, v_new: torch.Tensor,
 # ------------------------------------------------------------------------------------------------
 # a4/a5: decode attention
 # ------------------------------------------------------------------------------------------------
+def decode_plan(cache: LayerCache, n_q_heads: int, seq_len_host=None) -> dict:
+    """The work plan decode_attention would use (kvt_decode_plan): kernel, CTAs, whole units per SM of the per-SM
+    plan (0: none), resident CTAs per SM."""
+    out = (ctypes.c_int32 * 4)()
+    _check(_lib.kvt_decode_plan(ctypes.byref(cache._c), n_q_heads, _host_i32(seq_len_host), out))
+    return {"kernel": "tensor-core" if out[0] == 1 else "generic", "ctas": int(out[1]), "sm_whole_units": int(out[2]),
+            "ctas_per_sm": int(out[3])}
+
+
 def decode_workspace_bytes(cache: LayerCache, n_q_heads: int, seq_len_host=None) -> int:
     out = ctypes.c_uint64()
     _check(_lib.kvt_decode_workspace_bytes(ctypes.byref(cache._c), n_q_heads, _host_i32(seq_len_host),

@@ -28,7 +28,7 @@ def test_exports_every_declared_symbol(kvt):
     for name in sorted(declared):
         assert hasattr(lib, name), f"libkvt.so does not export {name}"
     assert set(kvt.kvt.EXPORTED) == declared
-    assert kvt.ABI_VERSION == 3          # 2: paged tile records; 3: kvt_append_decode_attention, counters first
+    assert kvt.ABI_VERSION == 4          # 2: paged records; 3: append+decode, counters first; 4: schedule counters, kvt_decode_plan
 
 
 def test_status_strings(kvt):

@@ -139,3 +139,20 @@ def test_sm_plan_workspace_shared_with_stream_k(kvt, oracle):
     assert words[:n_ctr + n_sched].abs().sum().item() == 0
     lens, K, V, q, _ = cases[0]
     _check_all(oracle, specs[0], lens, K, V, q, outs[0], H, g)
+
+
+def test_decode_plan_reports_the_launch(kvt):
+    """kvt_decode_plan: the Llama shape at B = 64 (512 units) runs the per-SM plan with 3 whole units per SM and one
+    full wave of CTAs; the Qwen shape (256 units, w = 1) and a small batch do not."""
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    c = kvt.LayerCache(kvt.LayerSpec.kivi(4, 2), 64, 8, D, 256)
+    p = kvt.decode_plan(c, 32)
+    assert p["kernel"] == "tensor-core"
+    if 512 // sms >= 2 and 512 % sms and 512 // sms + 1 <= p["ctas_per_sm"]:
+        assert p["sm_whole_units"] == 512 // sms and p["ctas"] == p["ctas_per_sm"] * sms
+    q = kvt.decode_plan(kvt.LayerCache(kvt.LayerSpec.kivi(4, 4), 64, 4, D, 256), 28)
+    assert q["sm_whole_units"] == 0
+    small = kvt.decode_plan(kvt.LayerCache(kvt.LayerSpec.kivi(4, 2), 2, 2, D, 256), 8)
+    assert small["sm_whole_units"] == 0 and small["ctas"] >= 1
+    g = kvt.decode_plan(kvt.LayerCache(kvt.LayerSpec.per_token(4, 4, group=64), 2, 2, D, 256), 8)
+    assert g["kernel"] == "generic"
