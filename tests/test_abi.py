@@ -142,3 +142,21 @@ def test_page_bytes():
     for spec in (kvt.LayerSpec.kivi(16, 4), kvt.LayerSpec.per_token(4, 4, group=64)):
         with pytest.raises(kvt.KvtError):
             kvt.page_bytes(spec, 8)
+
+
+def test_decode_workspace_layout_bound(kvt):
+    """include/kvt.h: [merge counters round_up(4 B H, 256)][schedule counters round_up(4 (514 + B H + SMs), 256)]
+    [partials].  Without a GPU the library plans for 4 CTAs/SM on 148 SMs; the Llama shape at B = 64 then uses the
+    per-SM plan (3 whole units + one piece per SM: 148 partial slots of 2 x 8 x (128 + 2) floats)."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("checks the host-only planning fallback")
+    B, H = 64, 8
+    c = kvt.LayerCache(kvt.LayerSpec.kivi(4, 2), B, H, 128, 64, device="cpu")
+    nb = kvt.decode_workspace_bytes(c, 32, None)
+    r256 = lambda x: (x + 255) // 256 * 256
+    assert nb == r256(4 * B * H) + r256(4 * (514 + B * H + 148)) + r256(148 * 2 * 8 * 130 * 4)
+    # a single sequence with one KV head runs as one whole unit: no workspace
+    one = kvt.LayerCache(kvt.LayerSpec.kivi(4, 2), 1, 1, 128, 64, device="cpu")
+    assert kvt.decode_workspace_bytes(one, 4, None) == 0
